@@ -1,0 +1,750 @@
+// The C-ABI (include/voxellate_b200.h) and the host-side orchestration of the
+// device pipeline:
+//
+//   H2D sites -> K0 ingest/validate -> [timed+prune: K1 bin, K6 prune] -> K1 bin
+//   -> param (r0 closed form | device t0 scan) -> K2 ball (+K3 compaction,
+//   +histogram) -> K4 shell search -> D2H labels / distances / histogram.
+//
+// Mirrors tessellate_fast (tessellate.cpp:195-282): the same input checks and
+// messages (check_inputs / SiteSet::validate, tessellate.cpp:176-180,
+// sites.cpp:41-59; override checks tessellate.cpp:221,231-232), and the same
+// output semantics (labels = original site indices after prune, Voronoi
+// distances = sqrt of the best squared distance, tessellate.cpp:160-164,272-280).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "voxellate_b200.h"
+#include "vx_internal.cuh"
+
+using namespace vxb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct Buf {
+  void* p = nullptr;
+  size_t n = 0;
+};
+
+}  // namespace
+
+struct vx_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  Buf pos_raw, t_raw, w_raw, p3, t, dropped, keys_a, keys_b, vals_a, vals_b, bx, by, bz, bt, bidx,
+      cell_start, cub, labels, dist, hist, unres, params, counters, scratch, vsample, vlab, vdist,
+      vbad;
+  DevParams* h_prm = nullptr;
+  DevCounters* h_ctr = nullptr;
+
+  Buf* all[28] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
+                  &vals_a,  &vals_b,  &bx,    &by,    &bz,     &bt,      &bidx,     &cell_start,
+                  &cub,     &labels,  &dist,  &hist,  &unres,  &params,  &counters, &scratch,
+                  &vsample, &vlab,    &vdist, &vbad};
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+struct CudaFail {
+  int code;
+  std::string msg;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw CudaFail{e == cudaErrorMemoryAllocation ? VX_ENOMEM : VX_ECUDA,
+                   std::string(what) + ": " + cudaGetErrorString(e)};
+  }
+}
+
+// VX_SYNC_DEBUG=1: synchronize after every stage and name the one that faulted.
+void dbg(cudaStream_t st, const char* stage) {
+  static const bool on = std::getenv("VX_SYNC_DEBUG") != nullptr;
+  if (!on) return;
+  ck(cudaStreamSynchronize(st), stage);
+  ck(cudaGetLastError(), stage);
+}
+
+template <class... A>
+int bin_checked(A&&... a) {
+  const int n = launch_bin(std::forward<A>(a)...);
+  if (n < 0) ck(static_cast<cudaError_t>(-1000 - n), "radix sort");
+  return n;
+}
+
+template <class T>
+T* ensure(Buf& b, size_t count) {
+  const size_t bytes = count * sizeof(T) + 16;
+  if (b.n < bytes) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.n = 0;
+    ck(cudaMalloc(&b.p, bytes), "cudaMalloc");
+    b.n = bytes;
+  }
+  return static_cast<T*>(b.p);
+}
+
+bool timed(const vx_problem* P) { return P->kind != VX_VORONOI; }
+
+// unit-ball volume, cost.cpp:15-22
+double unit_ball_volume(int d) { return std::pow(M_PI, 0.5 * d) / std::tgamma(0.5 * d + 1.0); }
+
+// radius_from_volume(optimal_v0(n, V), d), cost.cpp:28-39
+double optimal_r0(int64_t n_sites, int d, const double* L) {
+  double V = 1.0;
+  for (int i = 0; i < d; ++i) V *= L[i];
+  const double ns = static_cast<double>(n_sites);
+  const double v0 = V * (-std::expm1(-std::log(ns) / (ns - 1.0)));
+  return std::pow(v0 / unit_ball_volume(d), 1.0 / d);
+}
+
+// cover_radius, tessellate.cpp:25-30
+double cover_radius(int d, const double* L, bool periodic) {
+  double s = 0.0;
+  for (int i = 0; i < d; ++i) s += L[i] * L[i];
+  const double diag = std::sqrt(s);
+  return periodic ? 0.5 * diag : diag;
+}
+
+// Scalar input checks in the reference's order and wording.
+int check_problem(const vx_problem* P) {
+  if (!P) return fail(VX_EINVAL, "problem must not be NULL");
+  if (P->kind < 0 || P->kind > 2) return fail(VX_EINVAL, "unknown tessellation kind");
+  if (P->dim < 1) return fail(VX_EINVAL, "domain must have at least one axis");
+  if (P->dim > VX_MAX_DIM) return fail(VX_EINVAL, "domain dimension exceeds supported maximum (16)");
+  for (int i = 0; i < P->dim; ++i)
+    if (!(std::isfinite(P->lengths[i]) && P->lengths[i] > 0.0))
+      return fail(VX_EINVAL, "domain lengths must be positive");
+  for (int i = 0; i < P->dim; ++i)
+    if (P->counts[i] < 1) return fail(VX_EINVAL, "voxel counts must be positive");
+  if (P->n_sites < 1) return fail(VX_EINVAL, "site set must contain at least one site");
+  if (!P->positions) return fail(VX_EINVAL, "site position array has inconsistent size");
+  if (timed(P)) {
+    if (!P->times && !P->weights)
+      return fail(VX_EINVAL, "timed site set must carry one birth time per site");
+    if (!(std::isfinite(P->growth) && P->growth > 0.0))
+      return fail(VX_EINVAL, "growth rate G must be positive for timed tessellations");
+  }
+  if (P->n_sites >= 0xFFFFFFFFll) return fail(VX_EINVAL, "site count exceeds the 32-bit label range");
+  if (P->n_sites > 0x7FFFFFFFll)
+    return fail(VX_EUNSUPPORTED, "int32 labels need fewer than 2^31 sites");
+  double nv = 1.0;
+  for (int i = 0; i < P->dim; ++i) nv *= (double)P->counts[i];
+  if (nv > 9.0e18) return fail(VX_EINVAL, "voxel count overflows int64");
+  return VX_OK;
+}
+
+// SiteSet::validate position rule, sites.cpp:54-57 (host pointers only)
+int check_positions_host(const vx_problem* P) {
+  const int d = P->dim;
+  for (int64_t s = 0; s < P->n_sites; ++s)
+    for (int i = 0; i < d; ++i) {
+      const double v = P->positions[s * d + i];
+      if (!(std::isfinite(v) && v > 0.0 && v < P->lengths[i]))
+        return fail(VX_EINVAL, "site positions must lie strictly inside the domain");
+    }
+  return VX_OK;
+}
+
+double host_time(const vx_problem* P, int64_t s) {
+  return P->times ? P->times[s] : -(P->weights[s]) / P->growth;
+}
+
+void fill_geo(Geo& g, const vx_problem* P, int64_t zb, int64_t ze, int64_t n_for_cells) {
+  std::memset(&g, 0, sizeof(g));
+  g.kind = P->kind;
+  g.periodic = P->periodic ? 1 : 0;
+  g.dim = P->dim;
+  g.has_times = timed(P);
+  g.growth = timed(P) ? P->growth : 0.0;
+  g.g_is_one = g.growth == 1.0;
+  g.lmax = 0.0;
+  // true axis a -> embedded axis; the last true axis is always z (see Geo)
+  static const int kEmb[4][3] = {{0, 1, 2}, {2, 0, 0}, {0, 2, 0}, {0, 1, 2}};
+  const int dd = P->dim <= 3 ? P->dim : 3;
+  bool real[3] = {false, false, false};
+  for (int a = 0; a < 3; ++a) {
+    g.emb[a] = kEmb[dd][a];
+    g.n[a] = 1;
+    g.L[a] = 1.0;
+  }
+  for (int a = 0; a < dd; ++a) {
+    g.n[g.emb[a]] = P->counts[a];
+    g.L[g.emb[a]] = P->lengths[a];
+    real[g.emb[a]] = true;
+  }
+  g.vol_true = 1.0;
+  g.suml2_true = 0.0;
+  for (int a = 0; a < P->dim; ++a) {
+    g.vol_true *= P->lengths[a];
+    g.suml2_true += P->lengths[a] * P->lengths[a];
+  }
+  for (int a = 0; a < 3; ++a) {
+    g.invL[a] = 1.0 / g.L[a];                   // geometry.cpp:52
+    g.sp[a] = g.L[a] / (double)g.n[a];          // geometry.cpp:69
+    g.halfL[a] = 0.5 * g.L[a];
+    if (real[a]) g.lmax = std::fmax(g.lmax, g.L[a]);
+  }
+  // cell grid: about one site per cell, true axes only
+  const double V = g.vol_true;
+  double occ = 1.0;
+  if (const char* e = std::getenv("VX_CELL_OCC")) occ = std::atof(e);
+  double cw = std::pow(V * occ / (double)std::max<int64_t>(n_for_cells, 1), 1.0 / P->dim);
+  for (int iter = 0; iter < 64; ++iter) {
+    long long cells = 1;
+    for (int a = 0; a < 3; ++a) {
+      g.m[a] = real[a] ? (int)std::min(4096.0, std::max(1.0, std::floor(g.L[a] / cw))) : 1;
+      cells *= g.m[a];
+    }
+    g.n_cells = cells;
+    if (cells <= (1ll << 26)) break;
+    cw *= 1.25;
+  }
+  for (int a = 0; a < 3; ++a) {
+    g.cw[a] = g.L[a] / g.m[a];
+    g.inv_cw[a] = g.m[a] / g.L[a];
+  }
+  g.z_begin = zb;
+  g.z_end = ze;
+  g.nbx = (g.n[0] + BX - 1) / BX;
+  g.nby = (g.n[1] + BY - 1) / BY;
+  g.nbz = (ze - zb + BZ - 1) / BZ;
+  g.n_sites = P->n_sites;
+}
+
+std::map<int, std::unique_ptr<vx_context>>& thread_contexts() {
+  thread_local std::map<int, std::unique_ptr<vx_context>> m;
+  return m;
+}
+
+int create_context(int device, vx_context** out) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(VX_ECUDA, "no CUDA device available");
+  }
+  if (device < 0 || device >= ndev) return fail(VX_EINVAL, "invalid CUDA device ordinal");
+  DeviceGuard guard(device);
+  std::unique_ptr<vx_context> c(new vx_context);
+  c->device = device;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMallocHost(&c->h_prm, sizeof(DevParams)) != cudaSuccess ||
+      cudaMallocHost(&c->h_ctr, sizeof(DevCounters)) != cudaSuccess) {
+    const std::string m = cudaGetErrorString(cudaGetLastError());
+    return fail(VX_ECUDA, "context creation failed: " + m);
+  }
+  *out = c.release();
+  return VX_OK;
+}
+
+vx_context* resolve_context(vx_context* ctx, const vx_options* O, int* rc) {
+  *rc = VX_OK;
+  if (ctx) return ctx;
+  int dev = O && O->device >= 0 ? O->device : -1;
+  if (dev < 0) {
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      cudaGetLastError();
+      *rc = fail(VX_ECUDA, "no CUDA device available");
+      return nullptr;
+    }
+  }
+  auto& m = thread_contexts();
+  auto it = m.find(dev);
+  if (it != m.end()) return it->second.get();
+  vx_context* c = nullptr;
+  *rc = create_context(dev, &c);
+  if (*rc != VX_OK) return nullptr;
+  m[dev].reset(c);
+  return c;
+}
+
+int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t* labels_out,
+        vx_stats* stats, bool brute_engine) {
+  vx_options O;
+  if (O_in) O = *O_in;
+  else vx_options_init(&O);
+  int rc = check_problem(P);
+  if (rc) return rc;
+  if (!labels_out) return fail(VX_EINVAL, "labels_out must not be NULL");
+  const int d = P->dim;
+  const int64_t n_last = P->counts[d - 1];
+  int64_t zb = O.slab_begin, ze = O.slab_end;
+  if (zb == 0 && ze == 0) ze = n_last;
+  if (!(zb >= 0 && zb < ze && ze <= n_last))
+    return fail(VX_EINVAL, "slab must satisfy 0 <= slab_begin < slab_end <= counts[dim-1]");
+  if (O.asynchronous && !O.device_pointers)
+    return fail(VX_EINVAL, "asynchronous calls need device pointers");
+  const bool host_io = !O.device_pointers;
+  const bool do_prune = !brute_engine && timed(P) && O.prune;
+  const bool use_brute = brute_engine || d > 3;
+  double t_min_host = std::numeric_limits<double>::quiet_NaN();
+  if (host_io) {
+    if ((rc = check_positions_host(P))) return rc;
+    if (timed(P)) {
+      t_min_host = host_time(P, 0);
+      for (int64_t s = 1; s < P->n_sites; ++s) t_min_host = std::fmin(t_min_host, host_time(P, s));
+    }
+  }
+  if (!brute_engine && O.has_override) {
+    const double v = O.override_param;
+    if (!timed(P)) {
+      if (!(std::isfinite(v) && v > 0.0)) return fail(VX_EINVAL, "override r0 must be positive");
+    } else if (!std::isfinite(v) || (host_io && !(v >= t_min_host))) {
+      return fail(VX_EINVAL, "override t0 must not precede the earliest birth time");
+    }
+  }
+  double ball_scale = O.ball_scale > 0.0 ? O.ball_scale : 1.0;
+
+  vx_context* ctx = resolve_context(ctx_in, &O, &rc);
+  if (!ctx) return rc;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = O.stream ? static_cast<cudaStream_t>(O.stream) : ctx->stream;
+  int launches = 0;
+  int64_t plane = 1;
+  for (int i = 0; i < d - 1; ++i) plane *= P->counts[i];
+  const int64_t nvs = plane * (ze - zb);
+  const int64_t ns = P->n_sites;
+  try {
+    // ---- inputs ----
+    const double* pos = P->positions;
+    const double* times = P->times;
+    const double* weights = P->times ? nullptr : P->weights;
+    if (host_io) {
+      double* dp = ensure<double>(ctx->pos_raw, (size_t)ns * d);
+      ck(cudaMemcpyAsync(dp, pos, sizeof(double) * ns * d, cudaMemcpyHostToDevice, st), "H2D positions");
+      pos = dp;
+      if (timed(P)) {
+        const double* src = times ? times : weights;
+        double* dt = ensure<double>(times ? ctx->t_raw : ctx->w_raw, (size_t)ns);
+        ck(cudaMemcpyAsync(dt, src, sizeof(double) * ns, cudaMemcpyHostToDevice, st), "H2D times");
+        if (times) times = dt;
+        else weights = dt;
+      }
+    }
+    Geo g;
+    fill_geo(g, P, zb, ze, ns);
+    int32_t* lab = host_io ? ensure<int32_t>(ctx->labels, (size_t)nvs) : labels_out;
+    double* dist = nullptr;
+    if (O.distances_out) dist = host_io ? ensure<double>(ctx->dist, (size_t)nvs) : O.distances_out;
+    unsigned long long* hist = nullptr;
+    if (O.histogram_out) {
+      hist = host_io ? ensure<unsigned long long>(ctx->hist, (size_t)ns)
+                     : reinterpret_cast<unsigned long long*>(O.histogram_out);
+      ck(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * ns, st), "memset histogram");
+    }
+    g.vec_store = (g.n[0] % 4 == 0) && ((reinterpret_cast<uintptr_t>(lab) & 15) == 0);
+    DevParams* prm = ensure<DevParams>(ctx->params, 1);
+    DevCounters* ctr = ensure<DevCounters>(ctx->counters, 1);
+    double* tdev = timed(P) ? ensure<double>(ctx->t, (size_t)ns) : nullptr;
+    double* p3 = use_brute ? nullptr : ensure<double>(ctx->p3, (size_t)ns * 3);
+    Len16 len;
+    for (int i = 0; i < 16; ++i) len.L[i] = i < d ? P->lengths[i] : 1.0;
+    launches += launch_init(prm, ctr, st);
+    launches += launch_ingest(g, len, d, pos, times, weights, p3, tdev, ctr, st);
+    dbg(st, "ingest");
+
+    double r0 = std::numeric_limits<double>::quiet_NaN();
+    if (use_brute) {
+      uint8_t* dropped = nullptr;
+      if (do_prune) {
+        dropped = ensure<uint8_t>(ctx->dropped, (size_t)ns);
+        launches += launch_prune_generic(P->kind, P->periodic, d, P->lengths, g.growth, pos, tdev, ns,
+                                         dropped, st);
+      }
+      launches += launch_brute(P->kind, P->periodic, d, reinterpret_cast<const long long*>(P->counts), P->lengths, g.growth, pos, tdev,
+                               dropped, ns, zb * plane, ze * plane, lab, dist, hist, st);
+    } else {
+      Bins bins;
+      double* bx = ensure<double>(ctx->bx, (size_t)ns);
+      double* by = ensure<double>(ctx->by, (size_t)ns);
+      double* bz = ensure<double>(ctx->bz, (size_t)ns);
+      double* bt = timed(P) ? ensure<double>(ctx->bt, (size_t)ns) : nullptr;
+      int* bidx = ensure<int>(ctx->bidx, (size_t)ns);
+      int* cs = ensure<int>(ctx->cell_start, (size_t)g.n_cells + 1);
+      unsigned* ka = ensure<unsigned>(ctx->keys_a, (size_t)ns);
+      unsigned* kb = ensure<unsigned>(ctx->keys_b, (size_t)ns);
+      int* va = ensure<int>(ctx->vals_a, (size_t)ns);
+      int* vb = ensure<int>(ctx->vals_b, (size_t)ns);
+      const size_t cub_bytes = bin_tmp_bytes(ns);
+      void* cub = ensure<char>(ctx->cub, cub_bytes);
+      bins.x = bx;
+      bins.y = by;
+      bins.z = bz;
+      bins.t = bt;
+      bins.idx = bidx;
+      bins.cell_start = cs;
+      uint8_t* dropped = nullptr;
+      if (do_prune) {
+        dropped = ensure<uint8_t>(ctx->dropped, (size_t)ns);
+        launches += bin_checked(g, p3, tdev, nullptr, cub, cub_bytes, ka, kb, va, vb, bx, by, bz, bt,
+                               bidx, cs, prm, ctr, st);
+        dbg(st, "bin0");
+        launches += launch_prune(g, bins, p3, tdev, prm, dropped, st);
+        dbg(st, "prune");
+      }
+      launches += bin_checked(g, p3, tdev, dropped, cub, cub_bytes, ka, kb, va, vb, bx, by, bz, bt,
+                             bidx, cs, prm, ctr, st);
+      dbg(st, "bin");
+      if (std::getenv("VX_SYNC_DEBUG")) {  // host-side audit of the binning
+        std::vector<unsigned> hk((size_t)ns);
+        std::vector<int> hc((size_t)g.n_cells + 1), hv((size_t)ns);
+        ck(cudaMemcpy(hk.data(), kb, sizeof(unsigned) * ns, cudaMemcpyDeviceToHost), "dbg");
+        ck(cudaMemcpy(hv.data(), vb, sizeof(int) * ns, cudaMemcpyDeviceToHost), "dbg");
+        ck(cudaMemcpy(hc.data(), cs, sizeof(int) * (g.n_cells + 1), cudaMemcpyDeviceToHost), "dbg");
+        for (int64_t i = 1; i < ns; ++i)
+          if (hk[i] < hk[i - 1]) {
+            fprintf(stderr, "VXDBG keys unsorted at %ld: %u %u\n", (long)i, hk[i - 1], hk[i]);
+            break;
+          }
+        for (int64_t c = 1; c <= g.n_cells; ++c)
+          if (hc[c] < hc[c - 1] || hc[c] > ns) {
+            fprintf(stderr, "VXDBG cell_start bad at %ld: %d %d\n", (long)c, hc[c - 1], hc[c]);
+            break;
+          }
+        fprintf(stderr, "VXDBG ns %ld n_cells %lld m %d %d %d keys[0..3] %u %u %u vals %d %d cs_end %d\n",
+                (long)ns, g.n_cells, g.m[0], g.m[1], g.m[2], hk[0], hk[ns > 1], hk[ns > 2], hv[0],
+                hv[ns > 1], hc[g.n_cells]);
+      }
+      if (!timed(P)) r0 = ns == 1 ? cover_radius(d, P->lengths, P->periodic) : optimal_r0(ns, d, P->lengths);
+      double* scratch = ensure<double>(ctx->scratch, 1024);
+      launches += launch_params(g, bins, prm, ctr, O.has_override, O.override_param, r0,
+                                ball_scale, scratch, st);
+      const long long cap = (long long)std::min<int64_t>(nvs, 1ll << 22);
+      long long* unres = ensure<long long>(ctx->unres, (size_t)cap);
+      dbg(st, "params");
+      launches += launch_ball(g, bins, prm, lab, dist, hist, unres, cap, ctr, st);
+      dbg(st, "ball");
+      if (std::getenv("VX_SYNC_DEBUG")) {
+        std::vector<int> hc((size_t)g.n_cells + 1);
+        ck(cudaMemcpy(hc.data(), cs, sizeof(int) * (g.n_cells + 1), cudaMemcpyDeviceToHost), "dbg");
+        for (int64_t c = 1; c <= g.n_cells; ++c)
+          if (hc[c] < hc[c - 1] || hc[c] > ns) {
+            fprintf(stderr, "VXDBG after ball: cell_start bad at %ld: %d %d\n", (long)c, hc[c - 1], hc[c]);
+            break;
+          }
+        DevCounters hctr;
+        ck(cudaMemcpy(&hctr, ctr, sizeof(hctr), cudaMemcpyDeviceToHost), "dbg");
+        fprintf(stderr, "VXDBG after ball: n_unres %llu ball_evals %llu overflow %llu cap %lld\n",
+                hctr.n_unres, hctr.ball_evals, hctr.overflow_bricks, cap);
+      }
+      launches += launch_shell(g, bins, prm, lab, dist, hist, unres, cap, ctr, st);
+      dbg(st, "shell");
+    }
+    ck(cudaGetLastError(), "kernel launch");
+    if (host_io) {
+      ck(cudaMemcpyAsync(labels_out, lab, sizeof(int32_t) * nvs, cudaMemcpyDeviceToHost, st), "D2H labels");
+      if (dist)
+        ck(cudaMemcpyAsync(O.distances_out, dist, sizeof(double) * nvs, cudaMemcpyDeviceToHost, st),
+           "D2H distances");
+      if (hist)
+        ck(cudaMemcpyAsync(O.histogram_out, hist, sizeof(unsigned long long) * ns,
+                           cudaMemcpyDeviceToHost, st),
+           "D2H histogram");
+    }
+    if (stats) {
+      std::memset(stats, 0, sizeof(*stats));
+      stats->engine = use_brute ? 1 : 0;
+      stats->kernel_launches = launches;
+      stats->n_voxels = nvs;
+      stats->param = std::numeric_limits<double>::quiet_NaN();
+    }
+    if (O.asynchronous) return VX_OK;
+    ck(cudaMemcpyAsync(ctx->h_prm, prm, sizeof(DevParams), cudaMemcpyDeviceToHost, st), "D2H params");
+    ck(cudaMemcpyAsync(ctx->h_ctr, ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st), "D2H counters");
+    ck(cudaStreamSynchronize(st), "pipeline");
+    if (ctx->h_ctr->bad_site) return fail(VX_EINVAL, "site positions must lie strictly inside the domain");
+    if (!brute_engine && O.has_override && timed(P) && !use_brute &&
+        !(O.override_param >= dkey_inv(ctx->h_prm->tmin_key)))
+      return fail(VX_EINVAL, "override t0 must not precede the earliest birth time");
+    if (stats) {
+      if (!use_brute) {
+        stats->param = ctx->h_prm->param;
+        stats->n_sites_kept = (int64_t)ctx->h_ctr->n_alive;
+        stats->n_unresolved = (int64_t)ctx->h_ctr->n_unres;
+        stats->ball_evals = ctx->h_ctr->ball_evals;
+        stats->shell_evals = ctx->h_ctr->shell_evals;
+        stats->overflow_bricks = ctx->h_ctr->overflow_bricks;
+      } else {
+        stats->n_sites_kept = ns;
+        stats->shell_evals = (uint64_t)nvs * (uint64_t)ns;
+        if (!brute_engine && !timed(P))
+          stats->param = ns == 1 ? cover_radius(d, P->lengths, P->periodic) : optimal_r0(ns, d, P->lengths);
+      }
+    }
+  } catch (const CudaFail& f) {
+    return fail(f.code, f.msg);
+  }
+  return VX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint32_t vx_abi_version(void) { return VX_ABI_VERSION; }
+
+const char* vx_version_string(void) {
+  return "voxellate_b200 1.0 (sm_100a; ball/shell gather engine, exact f64 labels)";
+}
+
+const char* vx_last_error(void) { return g_err.c_str(); }
+
+void vx_options_init(vx_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->prune = 1;
+  o->device = -1;
+  o->ball_scale = 1.0;
+}
+
+int vx_context_create(int device, vx_context** out) {
+  if (!out) return fail(VX_EINVAL, "out must not be NULL");
+  return create_context(device, out);
+}
+
+void vx_context_destroy(vx_context* ctx) {
+  if (!ctx) return;
+  {
+    DeviceGuard guard(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (Buf* b : ctx->all)
+      if (b->p) {
+        cudaFree(b->p);
+        b->p = nullptr;
+        b->n = 0;
+      }
+    if (ctx->h_prm) cudaFreeHost(ctx->h_prm);
+    if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
+    cudaStreamDestroy(ctx->stream);
+  }
+  delete ctx;
+}
+
+int64_t vx_context_workspace_bytes(const vx_context* ctx) {
+  if (!ctx) return 0;
+  int64_t s = 0;
+  for (const Buf* b : ctx->all) s += (int64_t)b->n;
+  return s;
+}
+
+int vx_tessellate(vx_context* ctx, const vx_problem* problem, const vx_options* options,
+                  int32_t* labels_out, vx_stats* stats_out) {
+  return run(ctx, problem, options, labels_out, stats_out, false);
+}
+
+int vx_tessellate_brute(vx_context* ctx, const vx_problem* problem, const vx_options* options,
+                        int32_t* labels_out, vx_stats* stats_out) {
+  return run(ctx, problem, options, labels_out, stats_out, true);
+}
+
+int vx_prune(vx_context* ctx_in, const vx_problem* P, uint8_t* dropped_out, int64_t* n_removed) {
+  int rc = check_problem(P);
+  if (rc) return rc;
+  if (!timed(P)) return fail(VX_EINVAL, "pruning applies to timed tessellations only");
+  if (!dropped_out) return fail(VX_EINVAL, "dropped_out must not be NULL");
+  if ((rc = check_positions_host(P))) return rc;
+  vx_context* ctx = resolve_context(ctx_in, nullptr, &rc);
+  if (!ctx) return rc;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const int d = P->dim;
+  const int64_t ns = P->n_sites;
+  try {
+    double* pos = ensure<double>(ctx->pos_raw, (size_t)ns * d);
+    ck(cudaMemcpyAsync(pos, P->positions, sizeof(double) * ns * d, cudaMemcpyHostToDevice, st), "H2D");
+    double* src = ensure<double>(ctx->t_raw, (size_t)ns);
+    ck(cudaMemcpyAsync(src, P->times ? P->times : P->weights, sizeof(double) * ns,
+                       cudaMemcpyHostToDevice, st), "H2D");
+    Geo g;
+    fill_geo(g, P, 0, P->counts[d - 1], ns);
+    double* tdev = ensure<double>(ctx->t, (size_t)ns);
+    double* p3 = d <= 3 ? ensure<double>(ctx->p3, (size_t)ns * 3) : nullptr;
+    DevParams* prm = ensure<DevParams>(ctx->params, 1);
+    DevCounters* ctr = ensure<DevCounters>(ctx->counters, 1);
+    uint8_t* dropped = ensure<uint8_t>(ctx->dropped, (size_t)ns);
+    Len16 len;
+    for (int i = 0; i < 16; ++i) len.L[i] = i < d ? P->lengths[i] : 1.0;
+    launch_init(prm, ctr, st);
+    launch_ingest(g, len, d, pos, P->times ? src : nullptr, P->times ? nullptr : src, p3, tdev, ctr, st);
+    if (d <= 3) {
+      Bins bins;
+      double* bx = ensure<double>(ctx->bx, (size_t)ns);
+      double* by = ensure<double>(ctx->by, (size_t)ns);
+      double* bz = ensure<double>(ctx->bz, (size_t)ns);
+      double* bt = ensure<double>(ctx->bt, (size_t)ns);
+      int* bidx = ensure<int>(ctx->bidx, (size_t)ns);
+      int* cs = ensure<int>(ctx->cell_start, (size_t)g.n_cells + 1);
+      unsigned* ka = ensure<unsigned>(ctx->keys_a, (size_t)ns);
+      unsigned* kb = ensure<unsigned>(ctx->keys_b, (size_t)ns);
+      int* va = ensure<int>(ctx->vals_a, (size_t)ns);
+      int* vb = ensure<int>(ctx->vals_b, (size_t)ns);
+      const size_t cub_bytes = bin_tmp_bytes(ns);
+      void* cub = ensure<char>(ctx->cub, cub_bytes);
+      bins.x = bx; bins.y = by; bins.z = bz; bins.t = bt; bins.idx = bidx; bins.cell_start = cs;
+      bin_checked(g, p3, tdev, nullptr, cub, cub_bytes, ka, kb, va, vb, bx, by, bz, bt, bidx, cs, prm,
+                 ctr, st);
+      launch_prune(g, bins, p3, tdev, prm, dropped, st);
+    } else {
+      launch_prune_generic(P->kind, P->periodic, d, P->lengths, P->growth, pos, tdev, ns, dropped, st);
+    }
+    ck(cudaGetLastError(), "kernel launch");
+    ck(cudaMemcpyAsync(dropped_out, dropped, (size_t)ns, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "prune");
+  } catch (const CudaFail& f) {
+    return fail(f.code, f.msg);
+  }
+  int64_t removed = 0;
+  for (int64_t s = 0; s < ns; ++s) removed += dropped_out[s] ? 1 : 0;
+  if (n_removed) *n_removed = removed;
+  return VX_OK;
+}
+
+int vx_validate_partition(vx_context* ctx_in, const vx_problem* P, const int32_t* labels,
+                          const double* distances, int64_t sample, uint64_t seed,
+                          vx_validation* report) {
+  int rc = check_problem(P);
+  if (rc) return rc;
+  if (!labels || !report) return fail(VX_EINVAL, "labels and report must not be NULL");
+  if ((rc = check_positions_host(P))) return rc;
+  const int d = P->dim;
+  int64_t nv = 1;
+  for (int i = 0; i < d; ++i) nv *= P->counts[i];
+  std::vector<long long> chosen;
+  if (sample <= 0 || sample >= nv) {  // tessellate.cpp:321-330
+    chosen.resize((size_t)nv);
+    for (int64_t i = 0; i < nv; ++i) chosen[i] = i;
+  } else {
+    std::mt19937_64 eng(seed);
+    std::uniform_int_distribution<std::int64_t> pick(0, nv - 1);
+    chosen.resize((size_t)sample);
+    for (auto& c : chosen) c = pick(eng);
+  }
+  const int64_t n = (int64_t)chosen.size();
+  std::vector<int> lab_at((size_t)n), bad_l((size_t)n, 0), bad_v((size_t)n, 0);
+  std::vector<double> dist_at(distances ? (size_t)n : 0);
+  for (int64_t i = 0; i < n; ++i) {
+    lab_at[i] = labels[chosen[i]];
+    if (distances) dist_at[i] = distances[chosen[i]];
+  }
+  vx_context* ctx = resolve_context(ctx_in, nullptr, &rc);
+  if (!ctx) return rc;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const int64_t ns = P->n_sites;
+  try {
+    double* pos = ensure<double>(ctx->pos_raw, (size_t)ns * d);
+    ck(cudaMemcpyAsync(pos, P->positions, sizeof(double) * ns * d, cudaMemcpyHostToDevice, st), "H2D");
+    double* tdev = nullptr;
+    if (timed(P)) {
+      double* src = ensure<double>(ctx->t_raw, (size_t)ns);
+      ck(cudaMemcpyAsync(src, P->times ? P->times : P->weights, sizeof(double) * ns,
+                         cudaMemcpyHostToDevice, st), "H2D");
+      tdev = ensure<double>(ctx->t, (size_t)ns);
+      Geo g;
+      fill_geo(g, P, 0, P->counts[d - 1], ns);
+      Len16 len;
+      for (int i = 0; i < 16; ++i) len.L[i] = i < d ? P->lengths[i] : 1.0;
+      DevCounters* ctr = ensure<DevCounters>(ctx->counters, 1);
+      launch_ingest(g, len, d, pos, P->times ? src : nullptr, P->times ? nullptr : src, nullptr, tdev,
+                    ctr, st);
+    }
+    long long* ds = ensure<long long>(ctx->vsample, (size_t)n);
+    int* dl = ensure<int>(ctx->vlab, (size_t)n);
+    double* dd = distances ? ensure<double>(ctx->vdist, (size_t)n) : nullptr;
+    int* bad = ensure<int>(ctx->vbad, (size_t)(2 * n));
+    ck(cudaMemcpyAsync(ds, chosen.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaMemcpyAsync(dl, lab_at.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st), "H2D");
+    if (dd) ck(cudaMemcpyAsync(dd, dist_at.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaMemsetAsync(bad, 0, sizeof(int) * 2 * n, st), "memset");
+    launch_validate(P->kind, P->periodic, d, reinterpret_cast<const long long*>(P->counts), P->lengths, timed(P) ? P->growth : 0.0, pos,
+                    tdev, ns, ds, n, dl, dd, bad, bad + n, st);
+    ck(cudaGetLastError(), "kernel launch");
+    ck(cudaMemcpyAsync(bad_l.data(), bad, sizeof(int) * n, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaMemcpyAsync(bad_v.data(), bad + n, sizeof(int) * n, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "validate");
+  } catch (const CudaFail& f) {
+    return fail(f.code, f.msg);
+  }
+  std::memset(report, 0, sizeof(*report));
+  for (int64_t i = 0; i < n; ++i) {
+    ++report->voxels_checked;
+    const bool bl = bad_l[i] != 0, bv = distances && bad_v[i] != 0;
+    report->label_mismatches += bl;
+    report->value_mismatches += bv;
+    if ((bl || bv) && report->n_examples < 16) report->examples[report->n_examples++] = chosen[i];
+  }
+  return VX_OK;
+}
+
+int vx_optimal_r0(int64_t n_sites, int dim, const double* lengths, double* r0_out) {
+  if (n_sites < 2) return fail(VX_EINVAL, "optimal ball volume needs at least 2 sites");
+  if (dim < 1 || dim > VX_MAX_DIM || !lengths || !r0_out) return fail(VX_EINVAL, "bad arguments");
+  *r0_out = optimal_r0(n_sites, dim, lengths);
+  return VX_OK;
+}
+
+// sites.cpp:61-85 with std::mt19937_64 (the sequence is fixed by the standard)
+int vx_generate_uniform_sites(int dim, const double* lengths, int64_t n_sites, int kind,
+                              double growth, double horizon, uint64_t seed, double* positions_out,
+                              double* times_out) {
+  if (n_sites < 1) return fail(VX_EINVAL, "number of sites must be at least 1");
+  if (dim < 1 || dim > VX_MAX_DIM || !lengths || !positions_out) return fail(VX_EINVAL, "bad arguments");
+  if (kind != VX_VORONOI) {
+    if (!(growth > 0.0)) return fail(VX_EINVAL, "growth rate G must be positive for timed tessellations");
+    if (!(horizon > 0.0)) return fail(VX_EINVAL, "time horizon T must be positive");
+    if (!times_out) return fail(VX_EINVAL, "times_out must not be NULL for timed kinds");
+  }
+  std::mt19937_64 eng(seed);
+  auto u01 = [&eng] { return static_cast<double>(eng() >> 11) * 0x1.0p-53; };
+  for (int64_t s = 0; s < n_sites; ++s) {
+    for (int i = 0; i < dim; ++i) {
+      double u = u01();
+      while (u == 0.0) u = u01();
+      positions_out[s * dim + i] = u * lengths[i];
+    }
+    if (kind != VX_VORONOI) times_out[s] = u01() * horizon;
+  }
+  return VX_OK;
+}
+
+void vx_slab_bounds(int64_t n_last, int rank, int world, int64_t* begin_out, int64_t* end_out) {
+  if (world < 1) world = 1;
+  if (begin_out) *begin_out = n_last * rank / world;
+  if (end_out) *end_out = n_last * (rank + 1) / world;
+}
+
+}  // extern "C"

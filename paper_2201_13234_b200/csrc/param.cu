@@ -1,0 +1,172 @@
+// Parameter choice for the ball phase (reference: tessellate.cpp:217-260).
+//
+// Labels never depend on r0 / t0 (test_tessellate.cpp:
+// 218-246), so these only size the gather.  Voronoi uses the reference's
+// closed-form r0 (computed on the host with the reference's formula, cost.cpp:
+// 28-39).  For timed kinds the reference runs a serial 257-point scan plus 60
+// golden-section steps of growth_cost (cost.cpp:56-146); here the same cost
+// model is evaluated on the device, 256 candidate t0 per pass in parallel
+// (one CTA each), two passes (coarse bracket, then the neighbours of the best
+// point).  Everything stays in device memory: no host round trip.
+#include "vx_internal.cuh"
+
+namespace vxb {
+
+constexpr int kScan = 256;
+
+__global__ void init_kernel(DevParams* prm, DevCounters* ctr) {
+  prm->tmin_key = ~0ull;
+  prm->tmax_key = 0ull;
+  prm->t_min = prm->t_max = 0.0;
+  ctr->n_unres = ctr->ball_evals = ctr->shell_evals = ctr->overflow_bricks = 0;
+  ctr->n_alive = 0;
+  ctr->bad_site = 0;
+}
+
+__global__ void voronoi_params_kernel(DevParams* prm, double R, double lmax) {
+  prm->param = R;
+  prm->cutoff = R * R;
+  prm->gather_r = fmin(R * (1.0 + 1e-9) + 1e-12 * lmax, 4.0 * lmax);
+  prm->eps = 1e-12 * 3.0 * lmax * lmax;
+}
+
+struct CostArgs {
+  int kind, dim;
+  double growth, volume, unit;  // unit-ball volume in the true dimension
+  double width;                 // t0_bracket width (cost.cpp:78-96)
+};
+
+__device__ double site_frac(const CostArgs& a, double t0, double ts) {
+  const double dt = t0 - ts;
+  double r = 0.0;
+  if (dt > 0.0) r = a.kind == kJohnsonMehl ? a.growth * dt : sqrt(a.growth * dt);
+  double rd = 1.0;
+  for (int i = 0; i < a.dim; ++i) rd *= r;
+  const double v = fmin(a.volume, a.unit * rd);
+  return v / a.volume;
+}
+
+__device__ void scan_range(const CostArgs& a, const DevParams* prm, const double* costs0,
+                           int pass, double* lo, double* hi) {
+  const double t_min = dkey_inv(prm->tmin_key);
+  const double blo = t_min, bhi = t_min + a.width;
+  if (pass == 0) {
+    *lo = blo;
+    *hi = bhi;
+    return;
+  }
+  int best = 0;
+  for (int i = 1; i < kScan; ++i)
+    if (costs0[i] < costs0[best]) best = i;
+  const double step = (bhi - blo) / (kScan - 1);
+  const double bt = blo + (bhi - blo) * best / (kScan - 1);
+  *lo = fmax(blo, bt - step);
+  *hi = fmin(bhi, bt + step);
+}
+
+// growth_cost(t0)/N_v = sum v'_s/V + N_s * prod(1 - v'_s/V), one CTA per t0.
+__global__ void cost_scan_kernel(CostArgs a, const double* __restrict__ bt,
+                                 const DevCounters* ctr, const DevParams* prm, double* costs,
+                                 int pass) {
+  __shared__ double s_sum[32], s_log[32];
+  double lo, hi;
+  scan_range(a, prm, costs, pass, &lo, &hi);
+  const double t0 = lo + (hi - lo) * blockIdx.x / (kScan - 1);
+  const long long n = (long long)ctr->n_alive;
+  double sum = 0.0, lg = 0.0;
+  for (long long s = threadIdx.x; s < n; s += blockDim.x) {
+    const double f = site_frac(a, t0, bt[s]);
+    sum += f;
+    lg += log1p(-f);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    lg += __shfl_xor_sync(0xffffffffu, lg, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_sum[threadIdx.x >> 5] = sum;
+    s_log[threadIdx.x >> 5] = lg;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double S = 0.0, Lg = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      S += s_sum[w];
+      Lg += s_log[w];
+    }
+    costs[pass * kScan + blockIdx.x] = S + (double)n * exp(Lg);
+  }
+}
+
+__global__ void timed_finalize_kernel(CostArgs a, DevParams* prm, const DevCounters* ctr,
+                                      const double* costs, int has_override, double override_t0,
+                                      double lmax) {
+  const double t_min = dkey_inv(prm->tmin_key);
+  prm->t_min = t_min;
+  prm->t_max = dkey_inv(prm->tmax_key);
+  double t0;
+  if (has_override) {
+    t0 = override_t0;
+  } else if (ctr->n_alive <= 1) {
+    t0 = t_min + a.width;  // t0_bracket(...).hi, tessellate.cpp:232-233
+  } else {
+    double lo0, hi0, lo1, hi1;
+    scan_range(a, prm, costs, 0, &lo0, &hi0);
+    scan_range(a, prm, costs, 1, &lo1, &hi1);
+    int b0 = 0, b1 = 0;
+    for (int i = 1; i < kScan; ++i) {
+      if (costs[i] < costs[b0]) b0 = i;
+      if (costs[kScan + i] < costs[kScan + b1]) b1 = i;
+    }
+    t0 = costs[kScan + b1] <= costs[b0] ? lo1 + (hi1 - lo1) * b1 / (kScan - 1)
+                                        : lo0 + (hi0 - lo0) * b0 / (kScan - 1);
+  }
+  prm->param = t0;
+  prm->cutoff = t0;
+  double dt = t0 - t_min;
+  if (!(dt > 0.0)) dt = 0.0;
+  const double r = a.kind == kJohnsonMehl ? a.growth * dt : sqrt(a.growth * dt);
+  prm->gather_r = fmin(r * (1.0 + 1e-9) + 1e-12 * lmax, 4.0 * lmax);
+  const double tabs = fmax(fabs(prm->t_min), fabs(prm->t_max)) + fabs(t0);
+  prm->eps = 1e-12 * (tabs + (a.kind == kJohnsonMehl ? 2.0 * lmax / a.growth
+                                                      : 3.0 * lmax * lmax / a.growth));
+}
+
+int launch_params(const Geo& g, const Bins& bins, DevParams* prm, const DevCounters* ctr,
+                  int has_override, double override_param, double r0, double ball_scale,
+                  double* scratch, cudaStream_t st) {
+  if (g.kind == kVoronoi) {
+    const double R = has_override ? override_param : r0 * ball_scale;
+    voronoi_params_kernel<<<1, 1, 0, st>>>(prm, R, g.lmax);
+    return 1;
+  }
+  CostArgs a;
+  a.kind = g.kind;
+  a.dim = g.dim;
+  a.growth = g.growth;
+  const double sum_l2 = g.suml2_true;
+  a.volume = g.vol_true;
+  a.unit = pow(M_PI, 0.5 * g.dim) / tgamma(0.5 * g.dim + 1.0);
+  if (g.kind == kJohnsonMehl) {
+    const double reach = sqrt(sum_l2);
+    a.width = g.periodic ? reach / (2.0 * g.growth) : reach / g.growth;
+  } else {
+    a.width = g.periodic ? sum_l2 / (4.0 * g.growth) : sum_l2 / g.growth;
+  }
+  int n = 1;
+  if (!has_override) {
+    cost_scan_kernel<<<kScan, 256, 0, st>>>(a, bins.t, ctr, prm, scratch, 0);
+    cost_scan_kernel<<<kScan, 256, 0, st>>>(a, bins.t, ctr, prm, scratch, 1);
+    n += 2;
+  }
+  timed_finalize_kernel<<<1, 1, 0, st>>>(a, prm, ctr, scratch, has_override, override_param,
+                                         g.lmax);
+  return n;
+}
+
+int launch_init(DevParams* prm, DevCounters* ctr, cudaStream_t st) {
+  init_kernel<<<1, 1, 0, st>>>(prm, ctr);
+  return 1;
+}
+
+}  // namespace vxb

@@ -1,0 +1,216 @@
+// K4: widening-shell exact search for the voxels the ball phase left
+// unresolved (reference step 2: resolve_voxels_impl<K,P> with
+// only_unassigned=true, tessellate.cpp:36-75, an all-sites scan per voxel).
+//
+// One warp per voxel.  Ring r is the set of cells at Chebyshev distance r from
+// the voxel's cell (periodic axes wrap; an axis whose window reaches the whole
+// period is "full").  Each lane evaluates the exact reference ranking value of
+// the sites in its cells and keeps the lexicographic minimum of (prox, index)
+// -- the order-independent form of the reference's ascending strict-< scan.
+// After each ring the search stops once a conservative lower bound of prox over
+// every site outside the scanned window exceeds the current best (strictly, so
+// a tie with a lower-index site further out is still found).
+//
+// The unresolved list comes from the ball kernel's fused compaction.  If it
+// overflowed its capacity, the kernel instead compacts on the fly from the
+// label image (sentinel -1), which needs no host round trip.
+#include "vx_internal.cuh"
+
+namespace vxb {
+
+constexpr int kShellThreads = 256;
+
+__device__ __forceinline__ long long wrapm(long long c, long long m) {
+  const long long r = c % m;
+  return r < 0 ? r + m : r;
+}
+
+template <int KIND, bool PER>
+__device__ void shell_one(const Geo& g, const Bins& bins, const DevParams* prm, long long lin,
+                          int* labels, double* dist, unsigned long long* hist,
+                          unsigned long long* evals) {
+  const int lane = threadIdx.x & 31;
+  const long long kx = lin % g.n[0];
+  const long long ky = (lin / g.n[0]) % g.n[1];
+  const long long kz = lin / (g.n[0] * g.n[1]);
+  const double c[3] = {center(kx, g.sp[0]), center(ky, g.sp[1]), center(kz, g.sp[2])};
+  long long cv[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    long long q = (long long)(c[a] * g.inv_cw[a]);
+    cv[a] = q < 0 ? 0 : (q >= g.m[a] ? g.m[a] - 1 : q);
+  }
+  const double t_min = prm->t_min;
+  const bool g1 = g.g_is_one;
+  double best = __longlong_as_double(0x7ff0000000000000ll);
+  int bi = 0x7fffffff;
+  unsigned long long ne = 0;
+  long long plo[3] = {0, 0, 0}, phi[3] = {-1, -1, -1};
+  bool pfull[3] = {false, false, false};
+  for (long long r = 0;; ++r) {
+    long long lo[3], hi[3];
+    bool full[3];
+    bool allfull = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = cv[a] - r;
+      hi[a] = cv[a] + r;
+      full[a] = false;
+      if (PER) {
+        if (hi[a] - lo[a] + 1 >= g.m[a]) {
+          lo[a] = 0;
+          hi[a] = g.m[a] - 1;
+          full[a] = true;
+        }
+      } else {
+        if (lo[a] < 0) lo[a] = 0;
+        if (hi[a] > g.m[a] - 1) hi[a] = g.m[a] - 1;
+        full[a] = lo[a] == 0 && hi[a] == g.m[a] - 1;
+      }
+      allfull &= full[a];
+    }
+    const long long sx = hi[0] - lo[0] + 1, sy = hi[1] - lo[1] + 1, sz = hi[2] - lo[2] + 1;
+    const long long ncell = sx * sy * sz;
+    for (long long f = lane; f < ncell; f += 32) {
+      const long long ix = lo[0] + f % sx, iy = lo[1] + (f / sx) % sy, iz = lo[2] + f / (sx * sy);
+      const long long w[3] = {PER ? wrapm(ix, g.m[0]) : ix, PER ? wrapm(iy, g.m[1]) : iy,
+                              PER ? wrapm(iz, g.m[2]) : iz};
+      if (r > 0) {  // skip cells of the previous window
+        bool inside = true;
+        const long long u[3] = {ix, iy, iz};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          bool in_a;
+          if (pfull[a]) in_a = true;
+          else if (PER) in_a = wrapm(w[a] - plo[a], g.m[a]) <= phi[a] - plo[a];
+          else in_a = u[a] >= plo[a] && u[a] <= phi[a];
+          inside &= in_a;
+        }
+        if (inside) continue;
+      }
+      const long long cell = w[0] + (long long)g.m[0] * (w[1] + (long long)g.m[1] * w[2]);
+      VXCHK(cell >= 0 && cell < g.n_cells, "cell %lld w %lld %lld %lld r %lld lin %lld", cell,
+            w[0], w[1], w[2], r, lin);
+      const int pb = bins.cell_start[cell], pe = bins.cell_start[cell + 1];
+      VXCHK(pb >= 0 && pe <= g.n_sites && pb <= pe, "pb %d pe %d", pb, pe);
+      for (int p = pb; p < pe; ++p) {
+        // reference fold: s = 0; s += w_z^2; s += w_y^2; s += w_x^2
+        const double az = axis_sq<PER>(bins.z[p], c[2], g.L[2], g.invL[2]);
+        const double ay = axis_sq<PER>(bins.y[p], c[1], g.L[1], g.invL[1]);
+        const double ax = axis_sq<PER>(bins.x[p], c[0], g.L[0], g.invL[0]);
+        const double dsq = __dadd_rn(__dadd_rn(az, ay), ax);
+        const double pr = prox_from_dsq<KIND>(dsq, g.growth, g1, KIND == kVoronoi ? 0.0 : bins.t[p]);
+        const int id = bins.idx[p];
+        if (pr < best || (pr == best && id < bi)) {
+          best = pr;
+          bi = id;
+        }
+        ++ne;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob < best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (allfull) break;
+    // distance from the voxel centre to the outside of the scanned window
+    double lbd = __longlong_as_double(0x7ff0000000000000ll);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (full[a]) continue;
+      if (PER || lo[a] > 0) lbd = fmin(lbd, c[a] - lo[a] * g.cw[a]);
+      if (PER || hi[a] < g.m[a] - 1) lbd = fmin(lbd, (hi[a] + 1) * g.cw[a] - c[a]);
+    }
+    lbd = lbd * (1.0 - 1e-9) - 1e-12 * g.lmax;
+    if (lbd > 0.0 && bi != 0x7fffffff) {
+      double lbp;
+      if (KIND == kVoronoi) lbp = lbd * lbd;
+      else if (KIND == kJohnsonMehl) lbp = lbd / g.growth + t_min;
+      else lbp = lbd * lbd / g.growth + t_min;
+      const double slack = KIND == kVoronoi ? 0.0 : 1e-12 * (fabs(t_min) + g.lmax * g.lmax / g.growth + g.lmax / g.growth);
+      if (lbp - slack > best) break;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      plo[a] = lo[a];
+      phi[a] = hi[a];
+      pfull[a] = full[a];
+    }
+  }
+  if (lane == 0) {
+    const long long out = lin - g.z_begin * g.n[0] * g.n[1];
+    VXCHK(out >= 0 && out < (g.z_end - g.z_begin) * g.n[0] * g.n[1] && bi >= 0 && bi < g.n_sites,
+          "out %lld bi %d lin %lld", out, bi, lin);
+    labels[out] = bi;
+    if (dist) dist[out] = KIND == kVoronoi ? __dsqrt_rn(best) : best;
+    if (hist) atomicAdd(&hist[bi], 1ull);
+  }
+  *evals += ne;
+}
+
+template <int KIND, bool PER>
+__global__ void __launch_bounds__(kShellThreads)
+    shell_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, int* __restrict__ labels,
+                 double* __restrict__ dist, unsigned long long* __restrict__ hist,
+                 const long long* __restrict__ unres, long long unres_cap, DevCounters* ctr) {
+  const long long nwarps = (long long)gridDim.x * (kShellThreads / 32);
+  const long long w = blockIdx.x * (long long)(kShellThreads / 32) + (threadIdx.x >> 5);
+  const long long n = (long long)ctr->n_unres;
+  unsigned long long ne = 0;
+  if (n <= unres_cap) {
+    for (long long i = w; i < n; i += nwarps) {
+      VXCHK(unres[i] >= 0 && unres[i] < g.n[0] * g.n[1] * g.n[2], "unres[%lld]=%lld n=%lld", i,
+            unres[i], n);
+      shell_one<KIND, PER>(g, bins, prm, unres[i], labels, dist, hist, &ne);
+    }
+  } else {
+    // overflow: compact directly from the image (label sentinel -1)
+    const long long nvs = (g.z_end - g.z_begin) * g.n[0] * g.n[1];
+    const long long base = g.z_begin * g.n[0] * g.n[1];
+    const int lane = threadIdx.x & 31;
+    for (long long c0 = w * 32; c0 < nvs; c0 += nwarps * 32) {
+      const long long v = c0 + lane;
+      const bool un = v < nvs && labels[v] == -1;
+      unsigned mask = __ballot_sync(0xffffffffu, un);
+      while (mask) {
+        const int src = __ffs(mask) - 1;
+        mask &= mask - 1;
+        shell_one<KIND, PER>(g, bins, prm, base + c0 + src, labels, dist, hist, &ne);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ne += __shfl_xor_sync(0xffffffffu, ne, o);
+  if ((threadIdx.x & 31) == 0 && ne) atomicAdd(&ctr->shell_evals, ne);
+}
+
+template <int KIND>
+static void launch_k(const Geo& g, const Bins& bins, const DevParams* prm, int* labels,
+                     double* dist, unsigned long long* hist, const long long* unres,
+                     long long cap, DevCounters* ctr, cudaStream_t st) {
+  const int blocks = 148 * 4;
+  if (g.periodic)
+    shell_kernel<KIND, true><<<blocks, kShellThreads, 0, st>>>(g, bins, prm, labels, dist, hist,
+                                                               unres, cap, ctr);
+  else
+    shell_kernel<KIND, false><<<blocks, kShellThreads, 0, st>>>(g, bins, prm, labels, dist, hist,
+                                                                unres, cap, ctr);
+}
+
+int launch_shell(const Geo& g, const Bins& bins, const DevParams* prm, int* labels, double* dist,
+                 unsigned long long* hist, const long long* unres, long long unres_cap,
+                 DevCounters* ctr, cudaStream_t st) {
+  switch (g.kind) {
+    case kVoronoi: launch_k<kVoronoi>(g, bins, prm, labels, dist, hist, unres, unres_cap, ctr, st); break;
+    case kJohnsonMehl: launch_k<kJohnsonMehl>(g, bins, prm, labels, dist, hist, unres, unres_cap, ctr, st); break;
+    default: launch_k<kLaguerre>(g, bins, prm, labels, dist, hist, unres, unres_cap, ctr, st); break;
+  }
+  return 1;
+}
+
+}  // namespace vxb
