@@ -70,7 +70,7 @@ typedef struct vx_options {
   void* stream;           /* cudaStream_t to run on; NULL = the context's stream */
   int32_t asynchronous;   /* 1: return after enqueueing (device_pointers only; stats
                              then carry no device-side counts) */
-  int32_t reserved0;
+  int32_t profile_stages; /* 1: record CUDA events around each stage -> stats.stage_ms */
   double* distances_out;  /* optional: ranking value image (Voronoi: Euclidean distance) */
   uint64_t* histogram_out;/* optional: n_sites voxel counts per label (grain volumes) */
   int64_t slab_begin;     /* last-axis slab [slab_begin, slab_end) to label;      */
@@ -89,7 +89,18 @@ typedef struct vx_stats {
   int32_t engine;          /* 0 = ball/shell engine, 1 = brute engine */
   int32_t kernel_launches; /* kernels this call enqueued */
   uint64_t overflow_bricks;/* bricks that fell back to the shell search */
+  /* with options.profile_stages (synchronous calls): device ms per stage, timed
+   * by CUDA events on the call's stream:
+   * [0] H2D+ingest [1] bin+prune [2] params [3] ball [4] shell [5] D2H */
+  float stage_ms[8];
 } vx_stats;
+
+#define VX_STAGE_INGEST 0
+#define VX_STAGE_BIN 1
+#define VX_STAGE_PARAMS 2
+#define VX_STAGE_BALL 3
+#define VX_STAGE_SHELL 4
+#define VX_STAGE_D2H 5
 
 /* ValidationReport (tessellate.hpp:70-76). */
 typedef struct vx_validation {
@@ -146,6 +157,13 @@ int vx_generate_uniform_sites(int dim, const double* lengths, int64_t n_sites, i
                               double* positions_out, double* times_out);
 /* the slab of the last axis owned by rank `rank` of `world` (tessellate.cpp:120-121) */
 void vx_slab_bounds(int64_t n_last, int rank, int world, int64_t* begin_out, int64_t* end_out);
+/* FNV-style label fingerprint: h ^= label; h *= 1099511628211 */
+uint64_t vx_label_fingerprint(const int32_t* labels, int64_t n);
+
+/* ---- measurement ---- */
+/* sustained f64 DADD and f32 FADD issue rates (adds/s) of `device`; the
+ * roofline denominator for the per-voxel evaluation kernels */
+int vx_probe_pipe_rates(int device, double* dadd_per_s, double* fadd_per_s);
 
 #ifdef __cplusplus
 }

@@ -41,7 +41,7 @@ class vx_options(C.Structure):
         ("device_pointers", C.c_int32),
         ("stream", C.c_void_p),
         ("asynchronous", C.c_int32),
-        ("reserved0", C.c_int32),
+        ("profile_stages", C.c_int32),
         ("distances_out", C.c_void_p),
         ("histogram_out", C.c_void_p),
         ("slab_begin", C.c_int64),
@@ -61,7 +61,17 @@ class vx_stats(C.Structure):
         ("engine", C.c_int32),
         ("kernel_launches", C.c_int32),
         ("overflow_bricks", C.c_uint64),
+        ("stage_ms", C.c_float * 8),
     ]
+
+
+STAGES = ("ingest", "bin", "params", "ball", "shell", "d2h")
+
+
+def stats_dict(st: "vx_stats") -> dict:
+    d = {k: getattr(st, k) for k, _ in vx_stats._fields_ if k != "stage_ms"}
+    d["stage_ms"] = {name: float(st.stage_ms[i]) for i, name in enumerate(STAGES)}
+    return d
 
 
 class vx_validation(C.Structure):
@@ -96,6 +106,8 @@ SIGNATURES = {
                                             C.c_uint64, _P, _P]),
     "vx_slab_bounds": (None, [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64),
                               C.POINTER(C.c_int64)]),
+    "vx_label_fingerprint": (C.c_uint64, [_P, C.c_int64]),
+    "vx_probe_pipe_rates": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 
 _lib = None

@@ -52,6 +52,7 @@ struct vx_context {
       vbad;
   DevParams* h_prm = nullptr;
   DevCounters* h_ctr = nullptr;
+  cudaEvent_t ev[8] = {};  // stage markers (options.profile_stages)
 
   Buf* all[28] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
                   &vals_a,  &vals_b,  &bx,    &by,    &bz,     &bt,      &bidx,     &cell_start,
@@ -86,6 +87,27 @@ void ck(cudaError_t e, const char* what) {
                    std::string(what) + ": " + cudaGetErrorString(e)};
   }
 }
+
+// CUDA-event stage markers on the call's stream (options.profile_stages).
+struct StageTimer {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  cudaEvent_t* ev = nullptr;
+  bool marked[8] = {};
+  void mark(int i) {
+    if (on) {
+      cudaEventRecord(ev[i], st);
+      marked[i] = true;
+    }
+  }
+  void fill(float* ms) const {
+    for (int i = 0; i < 7; ++i) {
+      float v = 0.f;
+      if (on && marked[i] && marked[i + 1]) cudaEventElapsedTime(&v, ev[i], ev[i + 1]);
+      if (i < 8) ms[i] = v;
+    }
+  }
+};
 
 // VX_SYNC_DEBUG=1: synchronize after every stage and name the one that faulted.
 void dbg(cudaStream_t st, const char* stage) {
@@ -336,7 +358,14 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
   for (int i = 0; i < d - 1; ++i) plane *= P->counts[i];
   const int64_t nvs = plane * (ze - zb);
   const int64_t ns = P->n_sites;
+  StageTimer tm;
   try {
+    tm.on = O.profile_stages && !O.asynchronous;
+    tm.st = st;
+    tm.ev = ctx->ev;
+    if (tm.on && !ctx->ev[0])
+      for (auto& e : ctx->ev) ck(cudaEventCreate(&e), "event");
+    tm.mark(0);
     // ---- inputs ----
     const double* pos = P->positions;
     const double* times = P->times;
@@ -374,6 +403,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
     launches += launch_init(prm, ctr, st);
     launches += launch_ingest(g, len, d, pos, times, weights, p3, tdev, ctr, st);
     dbg(st, "ingest");
+    tm.mark(1);
 
     double r0 = std::numeric_limits<double>::quiet_NaN();
     if (use_brute) {
@@ -383,8 +413,13 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
         launches += launch_prune_generic(P->kind, P->periodic, d, P->lengths, g.growth, pos, tdev, ns,
                                          dropped, st);
       }
-      launches += launch_brute(P->kind, P->periodic, d, reinterpret_cast<const long long*>(P->counts), P->lengths, g.growth, pos, tdev,
-                               dropped, ns, zb * plane, ze * plane, lab, dist, hist, st);
+      tm.mark(2);
+      tm.mark(3);
+      launches += launch_brute(P->kind, P->periodic, d, reinterpret_cast<const long long*>(P->counts),
+                               P->lengths, g.growth, pos, tdev, dropped, ns, zb * plane, ze * plane,
+                               lab, dist, hist, st);
+      tm.mark(4);
+      tm.mark(5);
     } else {
       Bins bins;
       double* bx = ensure<double>(ctx->bx, (size_t)ns);
@@ -399,68 +434,39 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       int* vb = ensure<int>(ctx->vals_b, (size_t)ns);
       const size_t cub_bytes = bin_tmp_bytes(ns);
       void* cub = ensure<char>(ctx->cub, cub_bytes);
+      double* scratch = ensure<double>(ctx->scratch, 1024);
+      const long long cap = (long long)std::min<int64_t>(nvs, 1ll << 22);
+      long long* unres = ensure<long long>(ctx->unres, (size_t)cap);
+      uint8_t* dropped = do_prune ? ensure<uint8_t>(ctx->dropped, (size_t)ns) : nullptr;
       bins.x = bx;
       bins.y = by;
       bins.z = bz;
       bins.t = bt;
       bins.idx = bidx;
       bins.cell_start = cs;
-      uint8_t* dropped = nullptr;
       if (do_prune) {
-        dropped = ensure<uint8_t>(ctx->dropped, (size_t)ns);
         launches += bin_checked(g, p3, tdev, nullptr, cub, cub_bytes, ka, kb, va, vb, bx, by, bz, bt,
-                               bidx, cs, prm, ctr, st);
+                                bidx, cs, prm, ctr, st);
         dbg(st, "bin0");
         launches += launch_prune(g, bins, p3, tdev, prm, dropped, st);
         dbg(st, "prune");
       }
       launches += bin_checked(g, p3, tdev, dropped, cub, cub_bytes, ka, kb, va, vb, bx, by, bz, bt,
-                             bidx, cs, prm, ctr, st);
+                              bidx, cs, prm, ctr, st);
       dbg(st, "bin");
-      if (std::getenv("VX_SYNC_DEBUG")) {  // host-side audit of the binning
-        std::vector<unsigned> hk((size_t)ns);
-        std::vector<int> hc((size_t)g.n_cells + 1), hv((size_t)ns);
-        ck(cudaMemcpy(hk.data(), kb, sizeof(unsigned) * ns, cudaMemcpyDeviceToHost), "dbg");
-        ck(cudaMemcpy(hv.data(), vb, sizeof(int) * ns, cudaMemcpyDeviceToHost), "dbg");
-        ck(cudaMemcpy(hc.data(), cs, sizeof(int) * (g.n_cells + 1), cudaMemcpyDeviceToHost), "dbg");
-        for (int64_t i = 1; i < ns; ++i)
-          if (hk[i] < hk[i - 1]) {
-            fprintf(stderr, "VXDBG keys unsorted at %ld: %u %u\n", (long)i, hk[i - 1], hk[i]);
-            break;
-          }
-        for (int64_t c = 1; c <= g.n_cells; ++c)
-          if (hc[c] < hc[c - 1] || hc[c] > ns) {
-            fprintf(stderr, "VXDBG cell_start bad at %ld: %d %d\n", (long)c, hc[c - 1], hc[c]);
-            break;
-          }
-        fprintf(stderr, "VXDBG ns %ld n_cells %lld m %d %d %d keys[0..3] %u %u %u vals %d %d cs_end %d\n",
-                (long)ns, g.n_cells, g.m[0], g.m[1], g.m[2], hk[0], hk[ns > 1], hk[ns > 2], hv[0],
-                hv[ns > 1], hc[g.n_cells]);
-      }
-      if (!timed(P)) r0 = ns == 1 ? cover_radius(d, P->lengths, P->periodic) : optimal_r0(ns, d, P->lengths);
-      double* scratch = ensure<double>(ctx->scratch, 1024);
+      tm.mark(2);
+      if (!timed(P))
+        r0 = ns == 1 ? cover_radius(d, P->lengths, P->periodic) : optimal_r0(ns, d, P->lengths);
       launches += launch_params(g, bins, prm, ctr, O.has_override, O.override_param, r0,
                                 ball_scale, scratch, st);
-      const long long cap = (long long)std::min<int64_t>(nvs, 1ll << 22);
-      long long* unres = ensure<long long>(ctx->unres, (size_t)cap);
       dbg(st, "params");
+      tm.mark(3);
       launches += launch_ball(g, bins, prm, lab, dist, hist, unres, cap, ctr, st);
       dbg(st, "ball");
-      if (std::getenv("VX_SYNC_DEBUG")) {
-        std::vector<int> hc((size_t)g.n_cells + 1);
-        ck(cudaMemcpy(hc.data(), cs, sizeof(int) * (g.n_cells + 1), cudaMemcpyDeviceToHost), "dbg");
-        for (int64_t c = 1; c <= g.n_cells; ++c)
-          if (hc[c] < hc[c - 1] || hc[c] > ns) {
-            fprintf(stderr, "VXDBG after ball: cell_start bad at %ld: %d %d\n", (long)c, hc[c - 1], hc[c]);
-            break;
-          }
-        DevCounters hctr;
-        ck(cudaMemcpy(&hctr, ctr, sizeof(hctr), cudaMemcpyDeviceToHost), "dbg");
-        fprintf(stderr, "VXDBG after ball: n_unres %llu ball_evals %llu overflow %llu cap %lld\n",
-                hctr.n_unres, hctr.ball_evals, hctr.overflow_bricks, cap);
-      }
+      tm.mark(4);
       launches += launch_shell(g, bins, prm, lab, dist, hist, unres, cap, ctr, st);
       dbg(st, "shell");
+      tm.mark(5);
     }
     ck(cudaGetLastError(), "kernel launch");
     if (host_io) {
@@ -473,6 +479,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
                            cudaMemcpyDeviceToHost, st),
            "D2H histogram");
     }
+    tm.mark(6);
     if (stats) {
       std::memset(stats, 0, sizeof(*stats));
       stats->engine = use_brute ? 1 : 0;
@@ -484,6 +491,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
     ck(cudaMemcpyAsync(ctx->h_prm, prm, sizeof(DevParams), cudaMemcpyDeviceToHost, st), "D2H params");
     ck(cudaMemcpyAsync(ctx->h_ctr, ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st), "D2H counters");
     ck(cudaStreamSynchronize(st), "pipeline");
+    if (stats) tm.fill(stats->stage_ms);
     if (ctx->h_ctr->bad_site) return fail(VX_EINVAL, "site positions must lie strictly inside the domain");
     if (!brute_engine && O.has_override && timed(P) && !use_brute &&
         !(O.override_param >= dkey_inv(ctx->h_prm->tmin_key)))

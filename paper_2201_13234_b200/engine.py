@@ -11,7 +11,7 @@ from __future__ import annotations
 import ctypes as C
 from typing import Optional, Sequence
 
-from ._lib import check, lib, vx_options, vx_problem, vx_stats
+from ._lib import check, lib, stats_dict, vx_options, vx_problem, vx_stats
 
 
 class Tessellator:
@@ -40,7 +40,7 @@ class Tessellator:
             positions, labels, times=None, growth: float = 0.0, slab=None, histogram=None,
             distances=None, prune: bool = True, override: Optional[float] = None,
             stream: Optional[int] = None, asynchronous: bool = False,
-            ball_scale: Optional[float] = None) -> dict:
+            ball_scale: Optional[float] = None, profile: bool = False) -> dict:
         """All tensor arguments are CUDA tensors (f64 positions/times/distances,
         int32 labels, int64 histogram) on this device.  Returns the stats dict
         (device-side counters are zero when ``asynchronous``)."""
@@ -66,6 +66,7 @@ class Tessellator:
         if stream is not None:
             O.stream = C.c_void_p(stream)
         O.asynchronous = 1 if asynchronous else 0
+        O.profile_stages = 1 if profile else 0
         if slab is not None:
             O.slab_begin, O.slab_end = int(slab[0]), int(slab[1])
         if histogram is not None:
@@ -77,4 +78,4 @@ class Tessellator:
         st = vx_stats()
         check(lib().vx_tessellate(self._ctx, C.byref(P), C.byref(O), C.c_void_p(labels.data_ptr()),
                                   C.byref(st)))
-        return {k: getattr(st, k) for k, _ in vx_stats._fields_}
+        return stats_dict(st)

@@ -29,7 +29,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import check, lib, vx_options, vx_problem, vx_stats, vx_validation
+from ._lib import check, lib, stats_dict, vx_options, vx_problem, vx_stats, vx_validation
 
 
 class Boundary(enum.Enum):
@@ -236,7 +236,8 @@ def _problem(sites: SiteSet, grid: VoxelGrid) -> vx_problem:
 
 
 def _run(engine: str, sites: SiteSet, grid: VoxelGrid, options: Optional[FastOptions],
-         distances: bool, histogram: bool, slab, device, ball_scale, context=None) -> TessResult:
+         distances: bool, histogram: bool, slab, device, ball_scale, context=None, out=None,
+         profile=False) -> TessResult:
     P = _problem(sites, grid)
     O = vx_options()
     lib().vx_options_init(C.byref(O))
@@ -253,7 +254,13 @@ def _run(engine: str, sites: SiteSet, grid: VoxelGrid, options: Optional[FastOpt
     O.slab_begin, O.slab_end = zb, ze
     plane = grid.voxel_count() // grid.counts[-1]
     nvs = plane * (ze - zb)
-    labels = np.empty(nvs, dtype=np.int32)
+    if out is not None:  # caller-provided (e.g. pinned) label buffer
+        labels = out.reshape(-1).view(np.int32)
+        if labels.size != nvs or not labels.flags.c_contiguous:
+            raise ValueError("out must be a contiguous buffer of the labelled voxel count")
+    else:
+        labels = np.empty(nvs, dtype=np.int32)
+    O.profile_stages = 1 if profile else 0
     dist = np.empty(nvs, dtype=np.float64) if distances else None
     hist = np.zeros(sites.count(), dtype=np.uint64) if histogram else None
     O.distances_out = _ptr(dist)
@@ -262,7 +269,7 @@ def _run(engine: str, sites: SiteSet, grid: VoxelGrid, options: Optional[FastOpt
     fn = lib().vx_tessellate if engine == "fast" else lib().vx_tessellate_brute
     check(fn(context, C.byref(P), C.byref(O), _ptr(labels), C.byref(st)))
     counters = EvalCounters(int(st.ball_evals), int(st.shell_evals))
-    stats = {k: getattr(st, k) for k, _ in vx_stats._fields_}
+    stats = stats_dict(st)
     return TessResult(LabelImage(grid, labels.view(np.uint32)),
                       DistanceImage(grid, dist) if dist is not None else None, counters,
                       float(st.param) if engine == "fast" else float("nan"), hist, stats)
@@ -270,11 +277,12 @@ def _run(engine: str, sites: SiteSet, grid: VoxelGrid, options: Optional[FastOpt
 
 def tessellate_fast(sites: SiteSet, grid: VoxelGrid, options: Optional[FastOptions] = None, *,
                     distances: bool = True, histogram: bool = False, slab=None, device=None,
-                    ball_scale=None, context=None) -> TessResult:
+                    ball_scale=None, context=None, out=None, profile=False) -> TessResult:
     """Two-step engine on the GPU (tessellate.cpp:195-282).  ``slab=(z0, z1)``
-    labels only last-axis planes [z0, z1) (the multi-GPU decomposition)."""
+    labels only last-axis planes [z0, z1) (the multi-GPU decomposition);
+    ``out`` receives the labels (e.g. a pinned host buffer)."""
     return _run("fast", sites, grid, options or FastOptions(), distances, histogram, slab, device,
-                ball_scale, context)
+                ball_scale, context, out, profile)
 
 
 def tessellate_brute(sites: SiteSet, grid: VoxelGrid, *, distances: bool = True,
