@@ -49,15 +49,15 @@ struct vx_context {
   std::mutex mu;
   Buf pos_raw, t_raw, w_raw, p3, t, dropped, keys_a, keys_b, vals_a, vals_b, bx, by, bz, bt, bidx,
       cell_start, cub, labels, dist, hist, unres, params, counters, scratch, vsample, vlab, vdist,
-      vbad;
+      vbad, slots;
   DevParams* h_prm = nullptr;
   DevCounters* h_ctr = nullptr;
   cudaEvent_t ev[8] = {};  // stage markers (options.profile_stages)
 
-  Buf* all[28] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
+  Buf* all[29] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
                   &vals_a,  &vals_b,  &bx,    &by,    &bz,     &bt,      &bidx,     &cell_start,
                   &cub,     &labels,  &dist,  &hist,  &unres,  &params,  &counters, &scratch,
-                  &vsample, &vlab,    &vdist, &vbad};
+                  &vsample, &vlab,    &vdist, &vbad,  &slots};
 };
 
 namespace {
@@ -461,7 +461,13 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
                                 ball_scale, scratch, st);
       dbg(st, "params");
       tm.mark(3);
-      launches += launch_ball(g, bins, prm, lab, dist, hist, unres, cap, ctr, st);
+      static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 2;
+      if (ball_ver == 1) {
+        launches += launch_ball(g, bins, prm, lab, dist, hist, unres, cap, ctr, st);
+      } else {
+        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 64);
+        launches += launch_ball2(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
+      }
       dbg(st, "ball");
       tm.mark(4);
       launches += launch_shell(g, bins, prm, lab, dist, hist, unres, cap, ctr, st);
