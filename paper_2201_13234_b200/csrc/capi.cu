@@ -461,9 +461,16 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
                                 ball_scale, scratch, st);
       dbg(st, "params");
       tm.mark(3);
-      static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 2;
+      static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 4;
+      static const int bzw = std::getenv("VX_BZW") ? std::atoi(std::getenv("VX_BZW")) : 4;
       if (ball_ver == 1) {
         launches += launch_ball(g, bins, prm, lab, dist, hist, unres, cap, ctr, st);
+      } else if (ball_ver == 4) {
+        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 64);
+        launches += launch_ball4(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
+      } else if (ball_ver == 3) {
+        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 64);
+        launches += launch_ball3(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, bzw, st);
       } else {
         unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 64);
         launches += launch_ball2(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
