@@ -83,15 +83,19 @@ __global__ void gather_kernel(long long n, const int* __restrict__ vals,
                               const double* __restrict__ p3, const double* __restrict__ t,
                               double* __restrict__ bx, double* __restrict__ by,
                               double* __restrict__ bz, double* __restrict__ bt,
-                              int* __restrict__ bidx) {
+                              int* __restrict__ bidx, float4* __restrict__ f4) {
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int s = vals[p];
-  bx[p] = p3[3 * (long long)s + 0];
-  by[p] = p3[3 * (long long)s + 1];
-  bz[p] = p3[3 * (long long)s + 2];
-  if (t) bt[p] = t[s];
+  const double x = p3[3 * (long long)s + 0], y = p3[3 * (long long)s + 1],
+               z = p3[3 * (long long)s + 2];
+  bx[p] = x;
+  by[p] = y;
+  bz[p] = z;
+  const double tv = t ? t[s] : 0.0;
+  if (t) bt[p] = tv;
   bidx[p] = s;
+  if (f4) f4[p] = make_float4((float)x, (float)y, (float)z, (float)tv);
 }
 
 __global__ void cell_start_kernel(long long n, long long n_cells, const unsigned* __restrict__ keys,
@@ -133,7 +137,8 @@ int launch_ingest(const Geo& g, const Len16& len, int dim_in, const double* pos_
 int launch_bin(const Geo& g, const double* p3, const double* t, const uint8_t* dropped,
                void* cub_tmp, size_t cub_tmp_bytes, unsigned* keys_a, unsigned* keys_b,
                int* vals_a, int* vals_b, double* bx, double* by, double* bz, double* bt,
-               int* bidx, int* cell_start, DevParams* prm, DevCounters* ctr, cudaStream_t st) {
+               int* bidx, float4* f4, int* cell_start, DevParams* prm, DevCounters* ctr,
+               cudaStream_t st) {
   const int T = 256;
   const unsigned nb = (unsigned)((g.n_sites + T - 1) / T);
   keys_kernel<<<nb, T, 0, st>>>(g, p3, t, dropped, keys_a, vals_a, prm);
@@ -142,7 +147,7 @@ int launch_bin(const Geo& g, const double* p3, const double* t, const uint8_t* d
                                                         vals_b, (int)g.n_sites, 0,
                                                         key_bits(g.n_cells), st);
   if (e != cudaSuccess) return -1000 - (int)e;
-  gather_kernel<<<nb, T, 0, st>>>(g.n_sites, vals_b, p3, t, bx, by, bz, bt, bidx);
+  gather_kernel<<<nb, T, 0, st>>>(g.n_sites, vals_b, p3, t, bx, by, bz, bt, bidx, f4);
   cell_start_kernel<<<(unsigned)((g.n_cells + 1 + T - 1) / T), T, 0, st>>>(g.n_sites, g.n_cells,
                                                                           keys_b, cell_start, ctr);
   return 3 + 2 * ((key_bits(g.n_cells) + 7) / 8);  // ours + CUB's onesweep passes (approx.)

@@ -49,15 +49,15 @@ struct vx_context {
   std::mutex mu;
   Buf pos_raw, t_raw, w_raw, p3, t, dropped, keys_a, keys_b, vals_a, vals_b, bx, by, bz, bt, bidx,
       cell_start, cub, labels, dist, hist, unres, params, counters, scratch, vsample, vlab, vdist,
-      vbad, slots;
+      vbad, slots, f4;
   DevParams* h_prm = nullptr;
   DevCounters* h_ctr = nullptr;
   cudaEvent_t ev[8] = {};  // stage markers (options.profile_stages)
 
-  Buf* all[29] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
+  Buf* all[30] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
                   &vals_a,  &vals_b,  &bx,    &by,    &bz,     &bt,      &bidx,     &cell_start,
                   &cub,     &labels,  &dist,  &hist,  &unres,  &params,  &counters, &scratch,
-                  &vsample, &vlab,    &vdist, &vbad,  &slots};
+                  &vsample, &vlab,    &vdist, &vbad,  &slots,  &f4};
 };
 
 namespace {
@@ -444,15 +444,17 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       bins.t = bt;
       bins.idx = bidx;
       bins.cell_start = cs;
+      float4* f4 = ensure<float4>(ctx->f4, (size_t)ns);
+      bins.f4 = f4;
       if (do_prune) {
         launches += bin_checked(g, p3, tdev, nullptr, cub, cub_bytes, ka, kb, va, vb, bx, by, bz, bt,
-                                bidx, cs, prm, ctr, st);
+                                bidx, f4, cs, prm, ctr, st);
         dbg(st, "bin0");
         launches += launch_prune(g, bins, p3, tdev, prm, dropped, st);
         dbg(st, "prune");
       }
       launches += bin_checked(g, p3, tdev, dropped, cub, cub_bytes, ka, kb, va, vb, bx, by, bz, bt,
-                              bidx, cs, prm, ctr, st);
+                              bidx, f4, cs, prm, ctr, st);
       dbg(st, "bin");
       tm.mark(2);
       if (!timed(P))
@@ -461,9 +463,13 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
                                 ball_scale, scratch, st);
       dbg(st, "params");
       tm.mark(3);
-      static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 4;
+      static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 5;
       static const int bzw = std::getenv("VX_BZW") ? std::atoi(std::getenv("VX_BZW")) : 4;
-      if (ball_ver == 1) {
+      static const int sy = std::getenv("VX_SY") ? std::atoi(std::getenv("VX_SY")) : 4;
+      if (ball_ver == 5) {
+        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 64);
+        launches += launch_ball5(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, sy, st);
+      } else if (ball_ver == 1) {
         launches += launch_ball(g, bins, prm, lab, dist, hist, unres, cap, ctr, st);
       } else if (ball_ver == 4) {
         unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 64);
@@ -635,8 +641,9 @@ int vx_prune(vx_context* ctx_in, const vx_problem* P, uint8_t* dropped_out, int6
       const size_t cub_bytes = bin_tmp_bytes(ns);
       void* cub = ensure<char>(ctx->cub, cub_bytes);
       bins.x = bx; bins.y = by; bins.z = bz; bins.t = bt; bins.idx = bidx; bins.cell_start = cs;
-      bin_checked(g, p3, tdev, nullptr, cub, cub_bytes, ka, kb, va, vb, bx, by, bz, bt, bidx, cs, prm,
-                 ctr, st);
+      bins.f4 = nullptr;
+      bin_checked(g, p3, tdev, nullptr, cub, cub_bytes, ka, kb, va, vb, bx, by, bz, bt, bidx,
+                  (float4*)nullptr, cs, prm, ctr, st);
       launch_prune(g, bins, p3, tdev, prm, dropped, st);
     } else {
       launch_prune_generic(P->kind, P->periodic, d, P->lengths, P->growth, pos, tdev, ns, dropped, st);
