@@ -1,0 +1,357 @@
+"""GPU parity: the CUDA engine through the C-ABI vs the oracle and the
+reference's golden fixtures.  Bit-exact labels AND f64 values everywhere
+(integer/index work; the f64 values are the reference's own expressions).
+
+Restates the reference's pinning tests:
+test_tessellate.cpp:55-86 (hand-checked), :178-216 and acceptance.cpp:49-113
+(fast == brute bitwise over random instances), :218-246 (extreme r0), :292-310
+(equal birth times -> Voronoi), :312-341 (validate_partition), :343-363
+(worker-count independence -> slab/GPU-count independence), test_sites.cpp
+:125-143,173-194 (coincident sites, prune preserves partitions), plus the five
+BASELINE configs against the reference's label fingerprints (App. B).
+"""
+import ctypes as C
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, fixture_names, fixture_problem, load_fixture, to_vx
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+def run_fast(p, **kw):
+    import paper_2201_13234_b200 as vx
+
+    sites, grid = to_vx(p)
+    opts = vx.FastOptions(override_param=kw.pop("override", None), prune=kw.pop("prune", True))
+    return vx.tessellate_fast(sites, grid, opts, **kw)
+
+
+def run_brute(p, **kw):
+    import paper_2201_13234_b200 as vx
+
+    sites, grid = to_vx(p)
+    return vx.tessellate_brute(sites, grid, **kw)
+
+
+@pytest.mark.parametrize("name", fixture_names("tess_"))
+def test_golden_fixtures(name):
+    fx = load_fixture(name)
+    p = fixture_problem(fx)
+    ov = float(fx["override"])
+    r = run_fast(p, prune=bool(fx["prune"]), override=None if np.isnan(ov) else ov)
+    assert np.array_equal(r.labels.labels, fx["labels"])
+    assert np.array_equal(bits(r.distances.values), bits(fx["values"]))
+    if p.kind == 0 and np.isnan(ov):
+        assert r.param == float(fx["param"])  # Voronoi r0 is the reference's value
+    if p.kind == 0 or not bool(fx["prune"]):
+        b = run_brute(p)  # tessellate_brute has no prune
+        assert np.array_equal(b.labels.labels, fx["labels"])
+        assert np.array_equal(bits(b.distances.values), bits(fx["values"]))
+
+
+@pytest.mark.parametrize("name", fixture_names("prune_"))
+def test_prune_matches_reference(name):
+    import paper_2201_13234_b200 as vx
+
+    fx = load_fixture(name)
+    p = fixture_problem(fx)
+    sites, grid = to_vx(p)
+    pr = vx.prune_ineffective_sites(sites, grid.domain)
+    assert np.array_equal(np.isin(np.arange(p.n_sites), pr.removed).astype(np.uint8), fx["dropped"])
+    assert pr.kept == sorted(pr.kept)
+
+
+def random_instance(rng, i, big=False):
+    import oracle
+
+    d = 1 + i % 4
+    kind = (i // 4) % 3
+    periodic = (i // 12) % 2 == 1
+    if big:
+        d = 3
+    L = rng.uniform(0.5, 2.0, d)
+    cap = {1: 512, 2: 48, 3: 16, 4: 8}[d]
+    counts = [64, 64, 64] if big else list(rng.integers(2, cap + 1, d))
+    ns = 1 if i % 37 == 0 else int(rng.integers(1, 500))
+    G = float(np.exp(rng.uniform(np.log(0.1), np.log(10.0)))) if kind else 0.0
+    pos, t = oracle.generate_uniform_sites(d, L, ns, kind, float(rng.uniform(0.5, 2.0)),
+                                           int(rng.integers(1 << 62)))
+    return oracle.Problem(kind, counts, L, periodic, pos, t, G)
+
+
+def test_random_instances_fast_equals_brute_equals_oracle(oracle_mod):
+    """acceptance.cpp:49-113 (criterion 1) restated: 200 seeded instances."""
+    rng = np.random.default_rng(20260814)
+    bad = []
+    for i in range(200):
+        p = random_instance(rng, i, big=(i % 50 == 13))
+        override = None
+        if i % 7 == 0:
+            override = (float(np.exp(rng.uniform(np.log(0.02), np.log(2.0)))) if p.kind == 0
+                        else float(p.times.min() + rng.uniform(0.0, 1.5)))
+        prune = i % 2 == 0
+        f = run_fast(p, prune=prune, override=override)
+        b = run_brute(p)
+        lab, dist = oracle_mod.brute(p)
+        if prune and p.kind != 0:  # the reference labels the prune survivors
+            dropped = oracle_mod.prune(p)
+            if dropped.any():
+                keep = np.nonzero(dropped == 0)[0]
+                q = oracle_mod.Problem(p.kind, p.counts, p.lengths, p.periodic,
+                                       p.positions.reshape(-1, p.dim)[keep].reshape(-1),
+                                       p.times[keep], p.growth)
+                l2, dist = oracle_mod.brute(q)
+                lab = keep[l2].astype(np.uint32)
+        ok = (np.array_equal(f.labels.labels, lab) and np.array_equal(bits(f.distances.values), bits(dist))
+              and np.array_equal(b.labels.labels, oracle_mod.brute(p)[0]))
+        if not ok:
+            bad.append((i, p.dim, p.kind, p.periodic, p.n_sites))
+    assert not bad, bad
+
+
+def test_hand_checked():
+    import oracle
+
+    r = run_fast(oracle.Problem(0, [8], [1.0], True, [0.25, 0.75]))
+    assert r.labels.labels.tolist() == [0, 0, 0, 0, 1, 1, 1, 1]
+    assert abs(r.distances.values[0] - 0.1875) < 1e-14 and abs(r.distances.values[7] - 0.1875) < 1e-14
+    r = run_brute(oracle.Problem(0, [4, 4], [1.0, 2.0], False, [0.3, 0.4]))
+    assert (r.labels.labels == 0).all() and r.stats["shell_evals"] == 16
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+def test_extreme_radii_give_identical_output(oracle_mod, periodic):
+    """test_tessellate.cpp:218-246: r0 = 1e9 / 1e-12 / cover -> same image."""
+    pos, _ = oracle_mod.generate_uniform_sites(2, np.array([1.3, 0.9]), 7, 0, 1.0, 31)
+    p = oracle_mod.Problem(0, [9, 8], [1.3, 0.9], periodic, pos)
+    lab, dist = oracle_mod.brute(p)
+    for r0 in (1e9, 1e-12, 0.5 * np.sqrt(1.3 ** 2 + 0.9 ** 2) * 1.001):
+        r = run_fast(p, override=r0)
+        assert np.array_equal(r.labels.labels, lab) and np.array_equal(bits(r.distances.values), bits(dist))
+    r = run_fast(p, override=1e-12)
+    assert r.stats["n_unresolved"] == p.n_voxels  # no ball reaches a voxel: all go to the shell
+
+
+def test_ball_radius_independence(oracle_mod):
+    """Labels never depend on the investigation radius."""
+    p = oracle_mod.baseline_config(1)
+    base = run_fast(p, distances=False).labels.labels
+    for scale in (0.3, 0.7, 1.5, 3.0):
+        r = run_fast(p, distances=False, ball_scale=scale)
+        assert np.array_equal(r.labels.labels, base)
+
+
+def test_equal_birth_times_degenerate_to_voronoi(oracle_mod):
+    """test_tessellate.cpp:292-310."""
+    rng = np.random.default_rng(404)
+    for trial in range(10):
+        d = 1 + trial % 3
+        L = rng.uniform(0.5, 2.0, d)
+        counts = list(rng.integers(2, {1: 64, 2: 16, 3: 8}[d] + 1, d))
+        pos, _ = oracle_mod.generate_uniform_sites(d, L, 15, 0, 1.0, int(rng.integers(1 << 60)))
+        periodic = trial % 2 == 1
+        ref = run_brute(oracle_mod.Problem(0, counts, L, periodic, pos)).labels.labels
+        for kind in (1, 2):
+            t = np.full(15, rng.uniform(-1.0, 1.0))
+            p = oracle_mod.Problem(kind, counts, L, periodic, pos, t, float(np.exp(rng.uniform(np.log(0.2), np.log(5.0)))))
+            assert np.array_equal(run_fast(p).labels.labels, ref)
+
+
+def test_coincident_sites_lower_index_wins(oracle_mod):
+    """test_sites.cpp:125-143: exact ties keep the lower index."""
+    for kind in (0, 1, 2):
+        pos = np.array([0.5, 0.5, 0.5, 0.5, 0.25, 0.75, 0.25, 0.75])
+        t = np.array([0.3, 0.3, 0.1, 0.1]) if kind else None
+        p = oracle_mod.Problem(kind, [10, 9], [1.0, 1.0], True, pos, t, 1.0 if kind else 0.0)
+        lab, dist = oracle_mod.brute(p)
+        for prune in (True, False):
+            r = run_fast(p, prune=prune)
+            assert np.array_equal(r.labels.labels, lab)
+            assert 1 not in r.labels.labels and 3 not in r.labels.labels
+
+
+def test_prune_on_off_same_partition(oracle_mod):
+    """test_sites.cpp:173-194 / acceptance.cpp:389-436 restated on the GPU."""
+    rng = np.random.default_rng(37)
+    for trial in range(24):
+        kind = 1 if trial % 2 else 2
+        periodic = (trial // 2) % 2 == 0
+        L = rng.uniform(0.5, 2.0, 2)
+        ns = 5 + int(rng.integers(60))
+        pos, t = oracle_mod.generate_uniform_sites(2, L, ns, kind, 1.0, int(rng.integers(1 << 60)))
+        p = oracle_mod.Problem(kind, [48, 48], L, periodic, pos, t,
+                               float(np.exp(rng.uniform(np.log(0.2), np.log(10.0)))))
+        a = run_fast(p, prune=True)
+        b = run_fast(p, prune=False)
+        assert np.array_equal(a.labels.labels, b.labels.labels)
+        dropped = oracle_mod.prune(p)
+        for s in np.nonzero(dropped)[0]:
+            assert s not in a.labels.labels
+
+
+def test_validate_partition_detects_tampering(oracle_mod):
+    """test_tessellate.cpp:312-341."""
+    import paper_2201_13234_b200 as vx
+
+    pos, t = oracle_mod.generate_uniform_sites(2, np.array([1.0, 1.3]), 30, 2, 1.0, 123)
+    p = oracle_mod.Problem(2, [24, 20], [1.0, 1.3], True, pos, t, 1.7)
+    sites, grid = to_vx(p)
+    r = vx.tessellate_fast(sites, grid)
+    full = vx.validate_partition(r.labels, r.distances, sites)
+    assert full.ok() and full.voxels_checked == grid.voxel_count()
+    sampled = vx.validate_partition(r.labels, r.distances, sites, 100, 9)
+    assert sampled.ok() and sampled.voxels_checked == 100
+    victim = 173
+    tampered = vx.LabelImage(grid, r.labels.labels.copy())
+    tampered.labels[victim] = (tampered.labels[victim] + 1) % sites.count()
+    bad = vx.validate_partition(tampered, r.distances, sites)
+    assert bad.label_mismatches == 1 and bad.value_mismatches == 0 and bad.examples == [victim]
+    dented = vx.DistanceImage(grid, r.distances.values.copy())
+    dented.values[victim] += 1e-3
+    bad = vx.validate_partition(r.labels, dented, sites)
+    assert bad.label_mismatches == 0 and bad.value_mismatches == 1
+    # the sampled voxel set is the reference's draw (mt19937_64 + libstdc++)
+    idx = oracle_mod.sample_indices(grid.voxel_count(), 100, 9)
+    bad = vx.validate_partition(tampered, None, sites, 100, 9)
+    assert bad.label_mismatches == int(np.count_nonzero(idx == victim))
+
+
+def test_slab_and_histogram_independence(oracle_mod):
+    """Worker-count independence (test_tessellate.cpp:343-363) -> GPU-count
+    independence: slabs concatenate to the full image, bit for bit."""
+    import paper_2201_13234_b200 as vx
+
+    pos, t = oracle_mod.generate_uniform_sites(3, np.array([1.0, 1.0, 1.0]), 300, 1, 0.1, 808)
+    p = oracle_mod.Problem(1, [40, 36, 45], [1.0, 1.0, 1.0], True, pos, t, 1.0)
+    full = run_fast(p, histogram=True)
+    assert full.histogram.sum() == p.n_voxels
+    assert np.array_equal(full.histogram, np.bincount(full.labels.labels, minlength=p.n_sites))
+    for world in (2, 3, 8):
+        parts, dists, hist = [], [], np.zeros(p.n_sites, dtype=np.uint64)
+        for r in range(world):
+            z0, z1 = vx.slab_bounds(45, r, world)
+            s = run_fast(p, histogram=True, slab=(z0, z1))
+            parts.append(s.labels.labels)
+            dists.append(s.distances.values)
+            hist += s.histogram
+        assert np.array_equal(np.concatenate(parts), full.labels.labels)
+        assert np.array_equal(bits(np.concatenate(dists)), bits(full.distances.values))
+        assert np.array_equal(hist, full.histogram)
+
+
+def test_weights_equal_times(oracle_mod):
+    """Laguerre input as weights w = r^2 (t = -(w)/G, sites.cpp:101)."""
+    import paper_2201_13234_b200 as vx
+    from paper_2201_13234_b200._lib import check, lib, vx_options, vx_problem
+
+    pos, radii = oracle_mod.generate_lognormal_spheres(400, 0.05, 0.3, 5)
+    G = 1.7
+    t = oracle_mod.spheres_to_timed(radii, G)
+    p = oracle_mod.Problem(2, [30, 31, 32], [1.0, 1.0, 1.0], True, pos, t, G)
+    ref = run_fast(p, distances=False).labels.labels
+    w = radii * radii
+    P = vx_problem()
+    P.kind, P.dim, P.periodic = 2, 3, 1
+    for i in range(3):
+        P.counts[i], P.lengths[i] = p.counts[i], 1.0
+    P.n_sites = 400
+    P.positions = pos.ctypes.data
+    P.weights = w.ctypes.data
+    P.growth = G
+    out = np.empty(p.n_voxels, dtype=np.int32)
+    check(lib().vx_tessellate(None, C.byref(P), None, out.ctypes.data_as(C.c_void_p), None))
+    assert np.array_equal(out.view(np.uint32), ref)
+
+
+def test_device_pointer_path_matches_host(oracle_mod):
+    import torch
+
+    from paper_2201_13234_b200.engine import Tessellator
+
+    p = oracle_mod.baseline_config(1)
+    host = run_fast(p, histogram=True)
+    eng = Tessellator(0)
+    pos = torch.from_numpy(p.positions).cuda()
+    lab = torch.empty(p.n_voxels, dtype=torch.int32, device="cuda")
+    hist = torch.zeros(p.n_sites, dtype=torch.int64, device="cuda")
+    dist = torch.empty(p.n_voxels, dtype=torch.float64, device="cuda")
+    st = eng.run(kind=0, counts=list(p.counts), lengths=list(p.lengths), periodic=True, positions=pos,
+                 labels=lab, histogram=hist, distances=dist,
+                 stream=torch.cuda.current_stream().cuda_stream, profile=True)
+    assert np.array_equal(lab.cpu().numpy().view(np.uint32), host.labels.labels)
+    assert np.array_equal(bits(dist.cpu().numpy()), bits(host.distances.values))
+    assert np.array_equal(hist.cpu().numpy().astype(np.uint64), host.histogram)
+    assert st["stage_ms"]["ball"] > 0.0
+    eng.close()
+
+
+def test_high_dimension_uses_brute_engine(oracle_mod):
+    rng = np.random.default_rng(5)
+    for kind in (0, 1, 2):
+        pos, t = oracle_mod.generate_uniform_sites(4, np.array([1.0, 0.7, 1.3, 0.9]), 23, kind, 0.7,
+                                                   int(rng.integers(1 << 60)))
+        p = oracle_mod.Problem(kind, [5, 4, 6, 3], [1.0, 0.7, 1.3, 0.9], kind != 1, pos, t, 1.3)
+        lab, dist = oracle_mod.brute(p)
+        r = run_fast(p, prune=False)
+        assert r.stats["engine"] == 1
+        assert np.array_equal(r.labels.labels, lab) and np.array_equal(bits(r.distances.values), bits(dist))
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_baseline_config_fingerprints(oracle_mod, k):
+    """Zero mismatched voxels on the five BASELINE configs: the label
+    fingerprint equals the reference's; cfg1 also full image."""
+    import paper_2201_13234_b200 as vx
+
+    p = oracle_mod.baseline_config(k)
+    r = run_fast(p, distances=False, histogram=True)
+    lab = np.ascontiguousarray(r.labels.labels).view(np.int32)
+    fp = "%016x" % vx.lib().vx_label_fingerprint(lab.ctypes.data_as(C.c_void_p), lab.size)
+    assert fp == oracle_mod.SURVEY_FINGERPRINTS[k]
+    assert int(r.histogram.sum()) == p.n_voxels
+    if k == 1:
+        ref, _ = oracle_mod.brute(p, distances=False)
+        assert np.array_equal(r.labels.labels, ref)
+
+
+@pytest.mark.parametrize("ver", [1, 2, 3, 4, 5, 6, 7])
+def test_every_ball_kernel_variant(ver):
+    """Each ball-kernel generation stays bit-exact (selected with VX_BALL)."""
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import oracle
+from conftest import to_vx
+import paper_2201_13234_b200 as vx
+rng = np.random.default_rng(99)
+for i in range(36):
+    d = 3 if i %% 3 else 2
+    kind = i %% 3; per = (i // 3) %% 2 == 0
+    L = rng.uniform(0.5, 2.0, d)
+    counts = list(rng.integers(2, 40 if d == 3 else 120, d))
+    pos, t = oracle.generate_uniform_sites(d, L, int(rng.integers(1, 400)), kind, 0.3, int(rng.integers(1 << 60)))
+    p = oracle.Problem(kind, counts, L, per, pos, t, 1.3 if kind else 0.0)
+    s, g = to_vx(p)
+    r = vx.tessellate_fast(s, g, vx.FastOptions(prune=False))
+    lab, dist = oracle.brute(p)
+    assert np.array_equal(r.labels.labels, lab), i
+    assert np.array_equal(r.distances.values.view(np.uint64), dist.view(np.uint64)), i
+cfg = oracle.baseline_config(1)
+s, g = to_vx(cfg)
+r = vx.tessellate_fast(s, g, distances=False)
+assert oracle.fingerprint(r.labels.labels) == oracle.SURVEY_FINGERPRINTS[1]
+print("ok")
+""" % (ROOT, os.path.join(ROOT, "tests"))
+    env = dict(os.environ, VX_BALL=str(ver))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
