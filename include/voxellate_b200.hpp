@@ -1,0 +1,251 @@
+// voxellate_b200.hpp -- the reference's C++ engine API over the C-ABI.
+//
+// Header-only shim with the signatures of the reference's
+//   voxellate::tessellate_fast / tessellate_brute   (include/voxellate/tessellate.hpp:47,59-60)
+//   voxellate::prune_ineffective_sites              (include/voxellate/sites.hpp:69)
+//   voxellate::validate_partition                   (include/voxellate/tessellate.hpp:81-84)
+//   voxellate::generate_uniform_sites               (include/voxellate/sites.hpp:48-49)
+// and value types with the same fields (Domain, VoxelGrid, SiteSet, FastOptions,
+// TessResult, ...), in namespace vxb200 so it can coexist with the reference in
+// one program.  Errors become the reference's exceptions: VX_EINVAL ->
+// std::invalid_argument (same message), anything else -> std::runtime_error.
+//
+// A caller of the reference switches with
+//     namespace voxellate = vxb200;   // and link libvoxellate_b200.so
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <limits>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "voxellate_b200.h"
+
+namespace vxb200 {
+
+enum class Boundary { Periodic, NonPeriodic };
+enum class Kind { Voronoi, JohnsonMehl, Laguerre };
+inline constexpr int kMaxDim = VX_MAX_DIM;
+inline constexpr std::uint32_t kUnassignedLabel = 0xFFFFFFFFu;
+
+namespace detail {
+inline void check(int rc) {
+  if (rc == VX_OK) return;
+  const std::string msg = vx_last_error();
+  if (rc == VX_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+}  // namespace detail
+
+struct Domain {
+  std::vector<double> lengths;
+  std::vector<double> inv_lengths;
+  Boundary boundary = Boundary::Periodic;
+  Domain() = default;
+  Domain(std::vector<double> l, Boundary b) : lengths(std::move(l)), boundary(b) {
+    if (lengths.empty()) throw std::invalid_argument("domain must have at least one axis");
+    if ((int)lengths.size() > kMaxDim)
+      throw std::invalid_argument("domain dimension exceeds supported maximum (16)");
+    for (double L : lengths) {
+      if (!(std::isfinite(L) && L > 0.0)) throw std::invalid_argument("domain lengths must be positive");
+      inv_lengths.push_back(1.0 / L);
+    }
+  }
+  int dim() const { return (int)lengths.size(); }
+  double volume() const {
+    double v = 1.0;
+    for (double L : lengths) v *= L;
+    return v;
+  }
+  bool periodic() const { return boundary == Boundary::Periodic; }
+};
+
+struct VoxelGrid {
+  std::vector<std::int64_t> counts;
+  Domain domain;
+  std::vector<double> spacing;
+  VoxelGrid() = default;
+  VoxelGrid(std::vector<std::int64_t> c, Domain d) : counts(std::move(c)), domain(std::move(d)) {
+    if ((int)counts.size() != domain.dim())
+      throw std::invalid_argument("grid counts must match domain dimension");
+    for (auto n : counts)
+      if (n < 1) throw std::invalid_argument("voxel counts must be positive");
+    for (int i = 0; i < dim(); ++i) spacing.push_back(domain.lengths[i] / (double)counts[i]);
+  }
+  int dim() const { return (int)counts.size(); }
+  std::int64_t voxel_count() const {
+    std::int64_t n = 1;
+    for (auto c : counts) n *= c;
+    return n;
+  }
+  double center_coord(int axis, std::int64_t k) const { return ((double)k + 0.5) * spacing[axis]; }
+};
+
+struct SiteSet {
+  Kind kind = Kind::Voronoi;
+  int dim = 0;
+  std::vector<double> positions;
+  std::vector<double> times;
+  double growth = 0.0;
+  std::int64_t count() const { return dim == 0 ? 0 : (std::int64_t)positions.size() / dim; }
+  bool timed() const { return kind != Kind::Voronoi; }
+  const double* pos(std::int64_t s) const { return positions.data() + s * dim; }
+};
+
+struct LabelImage {
+  VoxelGrid grid;
+  std::vector<std::uint32_t> labels;
+};
+struct DistanceImage {
+  VoxelGrid grid;
+  std::vector<double> values;
+};
+struct EvalCounters {  // this engine's counts: ball phase / shell phase evaluations
+  std::uint64_t step1_evals = 0;
+  std::uint64_t step2_evals = 0;
+  std::uint64_t total() const { return step1_evals + step2_evals; }
+};
+struct TessResult {
+  LabelImage labels;
+  DistanceImage distances;
+  EvalCounters counters;
+  double param = std::numeric_limits<double>::quiet_NaN();
+};
+struct FastOptions {
+  std::optional<double> override_param;
+  bool prune = true;
+};
+struct PruneResult {
+  SiteSet sites;
+  std::vector<std::int64_t> removed;
+  std::vector<std::int64_t> kept;
+};
+struct ValidationReport {
+  std::int64_t voxels_checked = 0;
+  std::int64_t label_mismatches = 0;
+  std::int64_t value_mismatches = 0;
+  std::vector<std::int64_t> examples;
+  bool ok() const { return label_mismatches == 0 && value_mismatches == 0; }
+};
+
+namespace detail {
+inline vx_problem problem(const SiteSet& s, const VoxelGrid& g) {
+  if (s.dim != g.dim()) throw std::invalid_argument("site dimension does not match the domain");
+  if (s.count() < 1) throw std::invalid_argument("site set must contain at least one site");
+  if ((std::int64_t)s.positions.size() != s.count() * s.dim)
+    throw std::invalid_argument("site position array has inconsistent size");
+  if (s.timed() && (std::int64_t)s.times.size() != s.count())
+    throw std::invalid_argument("timed site set must carry one birth time per site");
+  vx_problem P{};
+  P.kind = (int)s.kind;
+  P.dim = g.dim();
+  P.periodic = g.domain.periodic() ? 1 : 0;
+  for (int i = 0; i < g.dim(); ++i) {
+    P.counts[i] = g.counts[i];
+    P.lengths[i] = g.domain.lengths[i];
+  }
+  P.n_sites = s.count();
+  P.positions = s.positions.data();
+  P.times = s.timed() ? s.times.data() : nullptr;
+  P.growth = s.timed() ? s.growth : 0.0;
+  return P;
+}
+
+inline TessResult run(const SiteSet& s, const VoxelGrid& g, const FastOptions* o, bool brute) {
+  const vx_problem P = problem(s, g);
+  vx_options O;
+  vx_options_init(&O);
+  if (o) {
+    O.prune = o->prune ? 1 : 0;
+    if (o->override_param) {
+      O.has_override = 1;
+      O.override_param = *o->override_param;
+    }
+  }
+  TessResult r;
+  r.labels.grid = g;
+  r.distances.grid = g;
+  r.labels.labels.resize((size_t)g.voxel_count());
+  r.distances.values.resize((size_t)g.voxel_count());
+  O.distances_out = r.distances.values.data();
+  vx_stats st{};
+  int32_t* out = reinterpret_cast<int32_t*>(r.labels.labels.data());
+  check(brute ? vx_tessellate_brute(nullptr, &P, &O, out, &st) : vx_tessellate(nullptr, &P, &O, out, &st));
+  r.counters.step1_evals = st.ball_evals;
+  r.counters.step2_evals = st.shell_evals;
+  if (!brute) r.param = st.param;
+  return r;
+}
+}  // namespace detail
+
+// tessellate.hpp:59-60
+inline TessResult tessellate_fast(const SiteSet& sites, const VoxelGrid& grid,
+                                  const FastOptions& options = {}) {
+  return detail::run(sites, grid, &options, false);
+}
+// tessellate.hpp:47
+inline TessResult tessellate_brute(const SiteSet& sites, const VoxelGrid& grid) {
+  return detail::run(sites, grid, nullptr, true);
+}
+
+// sites.hpp:69
+inline PruneResult prune_ineffective_sites(const SiteSet& sites, const Domain& domain) {
+  if (!sites.timed()) throw std::invalid_argument("pruning applies to timed tessellations only");
+  VoxelGrid g(std::vector<std::int64_t>(domain.dim(), 1), domain);
+  const vx_problem P = detail::problem(sites, g);
+  std::vector<std::uint8_t> dropped((size_t)sites.count());
+  std::int64_t removed = 0;
+  detail::check(vx_prune(nullptr, &P, dropped.data(), &removed));
+  PruneResult out;
+  out.sites.kind = sites.kind;
+  out.sites.dim = sites.dim;
+  out.sites.growth = sites.growth;
+  for (std::int64_t s = 0; s < sites.count(); ++s) {
+    if (dropped[s]) {
+      out.removed.push_back(s);
+      continue;
+    }
+    out.kept.push_back(s);
+    out.sites.positions.insert(out.sites.positions.end(), sites.pos(s), sites.pos(s) + sites.dim);
+    out.sites.times.push_back(sites.times[s]);
+  }
+  return out;
+}
+
+// tessellate.hpp:81-84
+inline ValidationReport validate_partition(const LabelImage& labels, const DistanceImage* distances,
+                                           const SiteSet& sites, std::int64_t sample = 0,
+                                           std::uint64_t seed = 0) {
+  const vx_problem P = detail::problem(sites, labels.grid);
+  if ((std::int64_t)labels.labels.size() != labels.grid.voxel_count())
+    throw std::invalid_argument("label image size does not match its grid");
+  vx_validation rep{};
+  detail::check(vx_validate_partition(nullptr, &P, reinterpret_cast<const int32_t*>(labels.labels.data()),
+                                      distances ? distances->values.data() : nullptr, sample, seed, &rep));
+  ValidationReport r;
+  r.voxels_checked = rep.voxels_checked;
+  r.label_mismatches = rep.label_mismatches;
+  r.value_mismatches = rep.value_mismatches;
+  r.examples.assign(rep.examples, rep.examples + rep.n_examples);
+  return r;
+}
+
+// sites.hpp:48-49
+inline SiteSet generate_uniform_sites(const Domain& domain, std::int64_t n_sites, Kind kind,
+                                      double growth, double time_horizon, std::uint64_t seed) {
+  SiteSet s;
+  s.kind = kind;
+  s.dim = domain.dim();
+  s.growth = kind == Kind::Voronoi ? 0.0 : growth;
+  s.positions.resize((size_t)(n_sites * s.dim));
+  if (kind != Kind::Voronoi) s.times.resize((size_t)n_sites);
+  detail::check(vx_generate_uniform_sites(s.dim, domain.lengths.data(), n_sites, (int)kind, growth,
+                                          time_horizon, seed, s.positions.data(),
+                                          kind == Kind::Voronoi ? nullptr : s.times.data()));
+  return s;
+}
+
+}  // namespace vxb200

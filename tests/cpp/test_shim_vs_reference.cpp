@@ -1,0 +1,121 @@
+// TEST PROGRAM (infrastructure): the C++ shim (include/voxellate_b200.hpp, CUDA
+// engine) against the reference library itself (oracle/_ref, compiled from
+// /root/reference/proj/src), in one process, through their identical APIs.
+// Restates test_tessellate.cpp:178-216 (fast == brute bit for bit), :271-290
+// (override validation), :312-341 (validate_partition) and the prune tests of
+// test_sites.cpp:173-194.  Exit code 0 == all checks passed.
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+
+#include "voxellate/sites.hpp"
+#include "voxellate/tessellate.hpp"
+#include "voxellate_b200.hpp"
+
+namespace R = voxellate;
+namespace G = vxb200;
+
+static int failures = 0;
+#define CHECK(c)                                                         \
+  do {                                                                   \
+    if (!(c)) {                                                          \
+      std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #c);            \
+      ++failures;                                                        \
+    }                                                                    \
+  } while (0)
+
+static double uni(std::mt19937_64& e, double lo, double hi) {
+  return lo + (hi - lo) * ((double)(e() >> 11) * 0x1.0p-53);
+}
+
+int main() {
+  std::mt19937_64 eng(2024);
+  int instances = 0;
+  for (int trial = 0; trial < 120; ++trial) {
+    const int d = trial % 9 == 8 ? 4 : 1 + trial % 3;
+    const int kind = trial % 3;
+    const bool periodic = (trial / 3) % 2;
+    std::vector<double> L(d);
+    for (auto& x : L) x = uni(eng, 0.5, 2.0);
+    const std::int64_t cap = d == 1 ? 200 : (d == 2 ? 24 : (d == 3 ? 12 : 6));
+    std::vector<std::int64_t> counts(d);
+    for (auto& n : counts) n = 2 + (std::int64_t)(eng() % (cap - 1));
+    const std::int64_t ns = 1 + (std::int64_t)(eng() % 60);
+    const double growth = kind ? std::exp(uni(eng, std::log(0.1), std::log(10.0))) : 1.0;
+    const double horizon = uni(eng, 0.5, 2.0);
+    const std::uint64_t seed = eng();
+
+    R::Domain rbox(L, periodic ? R::Boundary::Periodic : R::Boundary::NonPeriodic);
+    R::VoxelGrid rgrid(counts, rbox);
+    R::SiteSet rs = R::generate_uniform_sites(rbox, ns, (R::Kind)kind, growth, horizon, seed);
+    G::Domain gbox(L, periodic ? G::Boundary::Periodic : G::Boundary::NonPeriodic);
+    G::VoxelGrid ggrid(counts, gbox);
+    G::SiteSet gs = G::generate_uniform_sites(gbox, ns, (G::Kind)kind, growth, horizon, seed);
+    CHECK(gs.positions == rs.positions && gs.times == rs.times);
+
+    R::FastOptions ro;
+    G::FastOptions go;
+    ro.prune = go.prune = (trial % 5) != 0;
+    if (trial % 4 == 0) {
+      const double v = kind == 0 ? uni(eng, 0.02, 2.0)
+                                 : *std::min_element(rs.times.begin(), rs.times.end()) + uni(eng, 0.0, 1.0);
+      ro.override_param = go.override_param = v;
+    }
+    const R::TessResult rf = R::tessellate_fast(rs, rgrid, ro);
+    const G::TessResult gf = G::tessellate_fast(gs, ggrid, go);
+    CHECK(gf.labels.labels == rf.labels.labels);
+    CHECK(std::memcmp(gf.distances.values.data(), rf.distances.values.data(),
+                      rf.distances.values.size() * sizeof(double)) == 0);
+    if (kind == 0 && !ro.override_param) CHECK(gf.param == rf.param);
+    const G::TessResult gb = G::tessellate_brute(gs, ggrid);
+    const R::TessResult rb = R::tessellate_brute(rs, rgrid);
+    CHECK(gb.labels.labels == rb.labels.labels);
+    CHECK(std::memcmp(gb.distances.values.data(), rb.distances.values.data(),
+                      rb.distances.values.size() * sizeof(double)) == 0);
+    if (kind != 0) {
+      const R::PruneResult rp = R::prune_ineffective_sites(rs, rbox);
+      const G::PruneResult gp = G::prune_ineffective_sites(gs, gbox);
+      CHECK(gp.removed == rp.removed && gp.kept == rp.kept);
+    }
+    ++instances;
+  }
+  // override validation throws std::invalid_argument (test_tessellate.cpp:271-290)
+  {
+    G::Domain box({1.0, 1.0}, G::Boundary::Periodic);
+    G::VoxelGrid grid({8, 8}, box);
+    G::SiteSet s = G::generate_uniform_sites(box, 4, G::Kind::Voronoi, 0.0, 1.0, 1);
+    G::FastOptions bad;
+    bad.override_param = 0.0;
+    bool threw = false;
+    try {
+      G::tessellate_fast(s, grid, bad);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+  // validate_partition reports agree with the reference on a tampered image
+  {
+    std::mt19937_64 e(123);
+    R::Domain rbox({1.0, 1.3}, R::Boundary::Periodic);
+    R::VoxelGrid rgrid({24, 20}, rbox);
+    R::SiteSet rs = R::generate_uniform_sites(rbox, 30, R::Kind::Laguerre, 1.3, 1.0, 77);
+    G::Domain gbox({1.0, 1.3}, G::Boundary::Periodic);
+    G::VoxelGrid ggrid({24, 20}, gbox);
+    G::SiteSet gs = G::generate_uniform_sites(gbox, 30, G::Kind::Laguerre, 1.3, 1.0, 77);
+    R::TessResult rr = R::tessellate_fast(rs, rgrid);
+    G::TessResult gr = G::tessellate_fast(gs, ggrid);
+    rr.labels.labels[173] = (rr.labels.labels[173] + 1) % 30;
+    gr.labels.labels[173] = (gr.labels.labels[173] + 1) % 30;
+    for (std::int64_t sample : {0, 100}) {
+      const R::ValidationReport a = R::validate_partition(rr.labels, &rr.distances, rs, sample, 9);
+      const G::ValidationReport b = G::validate_partition(gr.labels, &gr.distances, gs, sample, 9);
+      CHECK(a.voxels_checked == b.voxels_checked && a.label_mismatches == b.label_mismatches &&
+            a.value_mismatches == b.value_mismatches && a.examples == b.examples);
+    }
+  }
+  std::printf("%d instances, %d failures\n", instances, failures);
+  if (failures == 0) std::printf("ALL OK\n");
+  return failures == 0 ? 0 : 1;
+}
