@@ -361,7 +361,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-planes", type=int, default=32)
-    ap.add_argument("--ref-planes", type=int, default=4)
+    ap.add_argument("--ref-planes", type=int, default=32)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
