@@ -263,6 +263,7 @@ void fill_geo(Geo& g, const vx_problem* P, int64_t zb, int64_t ze, int64_t n_for
   g.nby = (g.n[1] + BY - 1) / BY;
   g.nbz = (ze - zb + BZ - 1) / BZ;
   g.n_sites = P->n_sites;
+  g.stats_on = std::getenv("VX_STATS") != nullptr;
 }
 
 std::map<int, std::unique_ptr<vx_context>>& thread_contexts() {
@@ -466,25 +467,28 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 2;
       static const int bzw = std::getenv("VX_BZW") ? std::atoi(std::getenv("VX_BZW")) : 4;
       static const int sy = std::getenv("VX_SY") ? std::atoi(std::getenv("VX_SY")) : 4;
-      if (ball_ver == 7) {
-        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 64);
+      if (ball_ver == 8) {
+        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
+        launches += launch_ball8(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
+      } else if (ball_ver == 7) {
+        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
         launches += launch_ball7(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
       } else if (ball_ver == 6) {
-        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 64);
+        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
         launches += launch_ball6(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
       } else if (ball_ver == 5) {
-        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 64);
+        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
         launches += launch_ball5(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, sy, st);
       } else if (ball_ver == 1) {
         launches += launch_ball(g, bins, prm, lab, dist, hist, unres, cap, ctr, st);
       } else if (ball_ver == 4) {
-        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 64);
+        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
         launches += launch_ball4(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
       } else if (ball_ver == 3) {
-        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 64);
+        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
         launches += launch_ball3(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, bzw, st);
       } else {
-        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 64);
+        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
         launches += launch_ball2(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
       }
       dbg(st, "ball");
@@ -516,6 +520,16 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
     ck(cudaMemcpyAsync(ctx->h_prm, prm, sizeof(DevParams), cudaMemcpyDeviceToHost, st), "D2H params");
     ck(cudaMemcpyAsync(ctx->h_ctr, ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st), "D2H counters");
     ck(cudaStreamSynchronize(st), "pipeline");
+    if (g.stats_on && ctx->slots.p) {  // VX_STATS diagnostics (ball kernel v8)
+      unsigned long long h[128];
+      ck(cudaMemcpy(h, ctx->slots.p, sizeof(h), cudaMemcpyDeviceToHost), "stats");
+      const double nc = h[66] ? (double)h[66] : 1.0, nb = h[68] ? (double)h[68] : 1.0,
+                   ns2 = h[70] ? (double)h[70] : 1.0;
+      fprintf(stderr,
+              "VX_STATS gathered/CTA raw %.1f kept %.1f | brick list %.1f | sub-brick list %.2f "
+              "(%llu CTAs, %llu bricks, %llu sub-bricks)\n",
+              h[64] / nc, h[65] / nc, h[67] / nb, h[69] / ns2, h[66], h[68], h[70]);
+    }
     if (stats) tm.fill(stats->stage_ms);
     if (ctx->h_ctr->bad_site) return fail(VX_EINVAL, "site positions must lie strictly inside the domain");
     if (!brute_engine && O.has_override && timed(P) && !use_brute &&
