@@ -33,7 +33,7 @@ namespace v8 {
 constexpr int kSB = 16;           // super-brick edge (voxels)
 constexpr int kB2Threads = 256;   // 8 warps, one 8^3 brick each
 constexpr int kTcap = 768;        // sites gathered per super-brick
-constexpr int kWcap = 128;        // brick-level survivors per warp
+constexpr int kWcap = 64;         // brick-level survivors per warp (2 slots per lane)
 constexpr int kFcap = 32;         // sub-brick survivors per warp (exact stage)
 constexpr int kRows2 = 256;       // cell rows per super-brick
 constexpr float kRel = 1e-5f;
@@ -63,6 +63,7 @@ struct Smem2 {
   int warp_tot[kB2Threads / 32];
   int n_total;
   int n_kept;
+  double cx[kSB], cy[kSB], cz[kSB];  // exact voxel centres of the super-brick
   WarpSmem w[kB2Threads / 32];
 };
 
@@ -306,6 +307,10 @@ __global__ void __launch_bounds__(kB2Threads, 3)
     }
   }
   if (tid == 0) S.n_kept = 0;
+  if (tid < 3 * kSB) {  // exact voxel centres (geometry.hpp:58-60)
+    const int a = tid / kSB, k = tid % kSB;
+    (a == 0 ? S.cx : a == 1 ? S.cy : S.cz)[k] = center(K0[a] + k, g.sp[a]);
+  }
   __syncthreads();
   const int Traw = S.n_total;
   bool cta_ok = rows_ok && Traw > 0;
@@ -383,7 +388,8 @@ __global__ void __launch_bounds__(kB2Threads, 3)
     const int o[3] = {x0, y0, z0}, n[3] = {nx, ny, nz};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      const double l = center(K0[a] + o[a], g.sp[a]), h = center(K0[a] + o[a] + n[a] - 1, g.sp[a]);
+      const double* ct = a == 0 ? S.cx : (a == 1 ? S.cy : S.cz);
+      const double l = ct[o[a]], h = ct[o[a] + n[a] - 1];
       B.c[a] = (float)(0.5 * (l + h) - cc[a]);
       B.h[a] = (float)(0.5 * (h - l)) * (1.f + kRel) + 2.f * e_d;
     }
@@ -457,48 +463,53 @@ __global__ void __launch_bounds__(kB2Threads, 3)
     int n2 = 0;
     if (brick_ok) {
       const FBox Bs = box_of(bxo, sy, sz, sext[0], sext[1], sext[2]);
-      // tau over the brick list
-      float my_ub = __int_as_float(0x7f800000);
-      int my_i = -1;
-      for (int i = lane; i < nW; i += 32) {
-        SiteF s;
-        const int f = ws.W[i];
-        fbounds<KIND, PER>(S.rel[f], S.flag[f], Bs, halfLf, invG, s);
-        if (s.ubp < my_ub) {
-          my_ub = s.ubp;
-          my_i = i;
-        }
-      }
+      // one bound evaluation per brick-list site, kept in registers (slots
+      // lane and lane + 32; nW <= 64)
+      const bool va = lane < nW, vb = lane + 32 < nW;
+      const int fa = va ? ws.W[lane] : 0, fb = vb ? ws.W[lane + 32] : 0;
+      const unsigned fla = va ? S.flag[fa] : 0u, flb = vb ? S.flag[fb] : 0u;
+      SiteF sa, sb;
+      fbounds<KIND, PER>(S.rel[fa], fla, Bs, halfLf, invG, sa);
+      if (vb) fbounds<KIND, PER>(S.rel[fb], flb, Bs, halfLf, invG, sb);
+      // packed (upper bound, slot) arg-min -> reference s0 and tau = its ubp
+      auto okey = [](float v) -> unsigned {
+        const unsigned b = __float_as_uint(v);
+        return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+      };
+      unsigned km = min(va ? ((okey(sa.ubp) & ~63u) | (unsigned)lane) : 0xffffffffu,
+                        vb ? ((okey(sb.ubp) & ~63u) | (unsigned)(lane + 32)) : 0xffffffffu);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, my_ub, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, my_i, o);
-        if (ov < my_ub || (ov == my_ub && oi < my_i)) {
-          my_ub = ov;
-          my_i = oi;
-        }
-      }
-      const float tau = my_ub;
-      const int f0 = ws.W[my_i];
+      for (int o = 16; o > 0; o >>= 1) km = min(km, __shfl_xor_sync(0xffffffffu, km, o));
+      const int r0 = (int)(km & 63u), rl = r0 & 31;
+      const bool rhi = r0 >= 32;
+      // broadcast the reference's bounds from its owner lane
       SiteF z;
-      const unsigned fl0 = S.flag[f0];
-      fbounds<KIND, PER>(S.rel[f0], fl0, Bs, halfLf, invG, z);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        z.v[a] = __shfl_sync(0xffffffffu, rhi ? sb.v[a] : sa.v[a], rl);
+        z.mn[a] = __shfl_sync(0xffffffffu, rhi ? sb.mn[a] : sa.mn[a], rl);
+        z.mx[a] = __shfl_sync(0xffffffffu, rhi ? sb.mx[a] : sa.mx[a], rl);
+      }
+      z.t = __shfl_sync(0xffffffffu, rhi ? sb.t : sa.t, rl);
+      z.lb = __shfl_sync(0xffffffffu, rhi ? sb.lb : sa.lb, rl);
+      z.ub = __shfl_sync(0xffffffffu, rhi ? sb.ub : sa.ub, rl);
+      const float tau = __shfl_sync(0xffffffffu, rhi ? sb.ubp : sa.ubp, rl);
+      const unsigned fl0 = __shfl_sync(0xffffffffu, rhi ? flb : fla, rl);
+      const bool ka = va && (lane == r0 || (sa.lbp <= tau &&
+                                            bisector_keep<KIND, PER>(sa, fla, z, fl0, Bs, halfLf, invG, e_d)));
+      const bool kb = vb && (lane + 32 == r0 || (sb.lbp <= tau &&
+                                                 bisector_keep<KIND, PER>(sb, flb, z, fl0, Bs, halfLf, invG, e_d)));
       bool over = false;
-      for (int i0 = 0; i0 < nW; i0 += 32) {
-        const int i = i0 + lane;
-        bool keep = false;
-        int f = -1;
-        if (i < nW) {
-          f = ws.W[i];
-          SiteF s;
-          const unsigned fl = S.flag[f];
-          fbounds<KIND, PER>(S.rel[f], fl, Bs, halfLf, invG, s);
-          keep = f == f0 ||
-                 (s.lbp <= tau && bisector_keep<KIND, PER>(s, fl, z, fl0, Bs, halfLf, invG, e_d));
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, keep);
+      {
+        const unsigned m = __ballot_sync(0xffffffffu, ka);
         const int pos = n2 + __popc(m & ((1u << lane) - 1u));
-        if (keep && pos < kFcap) ws.F[pos] = f;
+        if (ka && pos < kFcap) ws.F[pos] = fa;
+        n2 += __popc(m);
+      }
+      {
+        const unsigned m = __ballot_sync(0xffffffffu, kb);
+        const int pos = n2 + __popc(m & ((1u << lane) - 1u));
+        if (kb && pos < kFcap) ws.F[pos] = fb;
         n2 += __popc(m);
       }
       over = n2 > kFcap;
@@ -523,14 +534,13 @@ __global__ void __launch_bounds__(kB2Threads, 3)
         for (int e = lane; e < n2 * 16; e += 32) {
           const int j = e >> 4, r = e & 15;
           const int p = S.p[ws.Fs[j]];
-          double w2;
-          if (r < 8)
-            w2 = axis_sq<PER>(bins.x[p], center(K0[0] + bxo + r, g.sp[0]), g.L[0], g.invL[0]);
-          else if (r < 12)
-            w2 = axis_sq<PER>(bins.y[p], center(K0[1] + sy + (r - 8), g.sp[1]), g.L[1], g.invL[1]);
-          else
-            w2 = axis_sq<PER>(bins.z[p], center(K0[2] + sz + (r - 12), g.sp[2]), g.L[2], g.invL[2]);
-          ws.T[j][r] = w2;
+          const int a = r < 8 ? 0 : (r < 12 ? 1 : 2);
+          const double* src = a == 0 ? bins.x : (a == 1 ? bins.y : bins.z);
+          const double c = a == 0 ? S.cx[bxo + r] : (a == 1 ? S.cy[sy + r - 8] : S.cz[sz + r - 12]);
+          const double u = __dsub_rn(src[p], c);
+          // |u| < 0.49 L: floor(u*invL + 0.5) == 0, so the reference's wrap is u itself
+          const double w = (!PER || fabs(u) < 0.49 * g.L[a]) ? u : wrap_delta(u, g.L[a], g.invL[a]);
+          ws.T[j][r] = __dmul_rn(w, w);
           if (r == 0 && KIND != kVoronoi) ws.Ft[j] = bins.t[p];
         }
         __syncwarp();
@@ -612,7 +622,7 @@ __global__ void __launch_bounds__(kB2Threads, 3)
       for (int i = 0; i < nun; ++i)
         if (off + i < unres_cap) unres[off + i] = mylins[i];
     }
-    evals += (unsigned long long)n2 * (sext[0] * sext[1] * sext[2]);
+    if (lane == 0) evals += (unsigned long long)n2 * (sext[0] * sext[1] * sext[2]);
     if (hist && n2 > 0) {
       __syncwarp();
       if (lane < n2 && ws.cnt[lane]) atomicAdd(&hist[ws.Fidx[lane]], (unsigned long long)ws.cnt[lane]);
