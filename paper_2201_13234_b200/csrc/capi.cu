@@ -464,10 +464,13 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
                                 ball_scale, scratch, st);
       dbg(st, "params");
       tm.mark(3);
-      static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 8;
+      static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 10;
       static const int bzw = std::getenv("VX_BZW") ? std::atoi(std::getenv("VX_BZW")) : 4;
       static const int sy = std::getenv("VX_SY") ? std::atoi(std::getenv("VX_SY")) : 4;
-      if (ball_ver == 9) {
+      if (ball_ver == 10) {
+        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
+        launches += launch_ball10(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
+      } else if (ball_ver == 9) {
         unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
         launches += launch_ball9(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
       } else if (ball_ver == 8) {

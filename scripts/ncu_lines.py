@@ -1,6 +1,6 @@
 """Summarise an ncu report's source page by CUDA source line.
 
-python scripts/ncu_lines.py report.ncu-rep [top]
+python scripts/ncu_lines.py report.ncu-rep [top | first-last]
 Prints the lines with the most warp-stall samples and executed instructions,
 plus the dominant stall reasons per line.
 """
@@ -12,7 +12,12 @@ import sys
 
 def main():
     rep = sys.argv[1]
-    top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+    rng = None
+    if len(sys.argv) > 2 and "-" in sys.argv[2]:  # a line range "a-b": print it in line order
+        rng = tuple(int(x) for x in sys.argv[2].split("-"))
+        top = 10 ** 9
+    else:
+        top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
                           "cuda,sass"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -52,7 +57,11 @@ def main():
             if v:
                 a["stalls"][c[6:]] = a["stalls"].get(c[6:], 0) + v
     print(f"total samples {total_s}")
-    for line, a in sorted(agg.items(), key=lambda kv: -kv[1]["samples"])[:top]:
+    items = sorted(agg.items(), key=lambda kv: -kv[1]["samples"])[:top]
+    if rng:
+        items = sorted((kv for kv in agg.items() if rng[0] <= kv[0] <= rng[1] and kv[1]["inst"]),
+                       key=lambda kv: kv[0])
+    for line, a in items:
         st = sorted(a["stalls"].items(), key=lambda kv: -kv[1])[:3]
         sts = " ".join(f"{k}={v}" for k, v in st)
         print(f"{line:5d} {100.0 * a['samples'] / max(total_s, 1):5.1f}% inst={a['inst']:>11d} "
