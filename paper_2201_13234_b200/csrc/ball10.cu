@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(kB2Threads, 3)
     atomicAdd(&eval_slots[64], (unsigned long long)Traw);
     atomicAdd(&eval_slots[65], (unsigned long long)T);
     atomicAdd(&eval_slots[66], 1ull);
+    atomicMax(&eval_slots[71], (unsigned long long)T);
   }
   cta_ok = cta_ok && T > 0 && T <= kTcap;
 
@@ -467,6 +468,7 @@ __global__ void __launch_bounds__(kB2Threads, 3)
     if (VX_STATS_ON && lane == 0) {
       atomicAdd(&eval_slots[67], (unsigned long long)nW);
       atomicAdd(&eval_slots[68], 1ull);
+      atomicMax(&eval_slots[72], (unsigned long long)nW);
     }
   }
   __syncwarp();
@@ -541,6 +543,7 @@ __global__ void __launch_bounds__(kB2Threads, 3)
       if (VX_STATS_ON && lane == 0) {
         atomicAdd(&eval_slots[69], (unsigned long long)n2);
         atomicAdd(&eval_slots[70], 1ull);
+        atomicMax(&eval_slots[73], (unsigned long long)n2);
       }
       if (over) n2 = 0;
       __syncwarp();

@@ -43,6 +43,8 @@ struct Buf {
 
 }  // namespace
 
+constexpr int kMaxChunks = 16;
+
 struct vx_context {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -53,6 +55,8 @@ struct vx_context {
   DevParams* h_prm = nullptr;
   DevCounters* h_ctr = nullptr;
   cudaEvent_t ev[8] = {};  // stage markers (options.profile_stages)
+  cudaStream_t copy_stream = nullptr;  // chunked D2H of host-buffer calls
+  cudaEvent_t chunk_ev[16] = {};
 
   Buf* all[30] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
                   &vals_a,  &vals_b,  &bx,    &by,    &bz,     &bt,      &bidx,     &cell_start,
@@ -360,6 +364,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
   const int64_t nvs = plane * (ze - zb);
   const int64_t ns = P->n_sites;
   StageTimer tm;
+  bool labels_copied = false;  // chunked D2H already issued
   try {
     tm.on = O.profile_stages && !O.asynchronous;
     tm.st = st;
@@ -467,48 +472,78 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 10;
       static const int bzw = std::getenv("VX_BZW") ? std::atoi(std::getenv("VX_BZW")) : 4;
       static const int sy = std::getenv("VX_SY") ? std::atoi(std::getenv("VX_SY")) : 4;
-      if (ball_ver == 10) {
+      auto ball_and_shell = [&](const Geo& gg, int32_t* lb, double* ds) {
         unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
-        launches += launch_ball10(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
-      } else if (ball_ver == 9) {
-        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
-        launches += launch_ball9(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
-      } else if (ball_ver == 8) {
-        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
-        launches += launch_ball8(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
-      } else if (ball_ver == 7) {
-        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
-        launches += launch_ball7(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
-      } else if (ball_ver == 6) {
-        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
-        launches += launch_ball6(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
-      } else if (ball_ver == 5) {
-        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
-        launches += launch_ball5(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, sy, st);
-      } else if (ball_ver == 1) {
-        launches += launch_ball(g, bins, prm, lab, dist, hist, unres, cap, ctr, st);
-      } else if (ball_ver == 4) {
-        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
-        launches += launch_ball4(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
-      } else if (ball_ver == 3) {
-        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
-        launches += launch_ball3(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, bzw, st);
-      } else {
-        unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
-        launches += launch_ball2(g, bins, prm, lab, dist, hist, unres, cap, ctr, slots, st);
+        if (ball_ver == 10) launches += launch_ball10(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
+        else if (ball_ver == 9) launches += launch_ball9(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
+        else if (ball_ver == 8) launches += launch_ball8(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
+        else if (ball_ver == 7) launches += launch_ball7(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
+        else if (ball_ver == 6) launches += launch_ball6(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
+        else if (ball_ver == 5) launches += launch_ball5(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, sy, st);
+        else if (ball_ver == 1) launches += launch_ball(gg, bins, prm, lb, ds, hist, unres, cap, ctr, st);
+        else if (ball_ver == 4) launches += launch_ball4(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
+        else if (ball_ver == 3) launches += launch_ball3(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, bzw, st);
+        else launches += launch_ball2(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
+        dbg(st, "ball");
+        tm.mark(4);
+        launches += launch_shell(gg, bins, prm, lb, ds, hist, unres, cap, ctr, st);
+        dbg(st, "shell");
+        tm.mark(5);
+      };
+      // Host-buffer calls: the slab is computed in z-chunks and each chunk's
+      // labels go to the host on a second stream while the next chunk is
+      // computed (the PCIe copy of the label image is the larger cost of such a
+      // call).  Chunks are whole super-bricks of the ball kernel (64 planes).
+      const int64_t nz = ze - zb;
+      int nchunk = 1;
+      if (host_io && !tm.on) {
+        const char* e = std::getenv("VX_CHUNKS");
+        nchunk = e ? std::max(1, std::min(kMaxChunks, std::atoi(e))) : (nz >= 256 ? 8 : 1);
       }
-      dbg(st, "ball");
-      tm.mark(4);
-      launches += launch_shell(g, bins, prm, lab, dist, hist, unres, cap, ctr, st);
-      dbg(st, "shell");
-      tm.mark(5);
+      const int64_t cz = nchunk > 1 ? ((nz + nchunk - 1) / nchunk + 63) / 64 * 64 : nz;
+      if (nchunk > 1 && !ctx->copy_stream) {
+        ck(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
+        for (auto& e : ctx->chunk_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      }
+      int ci = 0;
+      for (int64_t c0 = zb; c0 < ze; c0 += cz, ++ci) {
+        const int64_t c1 = std::min<int64_t>(ze, c0 + cz);
+        Geo gc = g;
+        gc.z_begin = c0;
+        gc.z_end = c1;
+        gc.nbz = (c1 - c0 + BZ - 1) / BZ;
+        int32_t* lb = lab + (c0 - zb) * plane;
+        double* ds = dist ? dist + (c0 - zb) * plane : nullptr;
+        gc.vec_store = (gc.n[0] % 4 == 0) && ((reinterpret_cast<uintptr_t>(lb) & 15) == 0);
+        if (ci > 0) launches += launch_chunk_roll(ctr, st);
+        ball_and_shell(gc, lb, ds);
+        if (nchunk > 1) {
+          cudaEvent_t ev = ctx->chunk_ev[ci % kMaxChunks];
+          ck(cudaEventRecord(ev, st), "chunk event");
+          ck(cudaStreamWaitEvent(ctx->copy_stream, ev, 0), "chunk wait");
+          ck(cudaMemcpyAsync(labels_out + (c0 - zb) * plane, lb, sizeof(int32_t) * (c1 - c0) * plane,
+                             cudaMemcpyDeviceToHost, ctx->copy_stream),
+             "D2H labels");
+          if (ds)
+            ck(cudaMemcpyAsync(O.distances_out + (c0 - zb) * plane, ds, sizeof(double) * (c1 - c0) * plane,
+                               cudaMemcpyDeviceToHost, ctx->copy_stream),
+               "D2H distances");
+        }
+      }
+      if (nchunk > 1) {  // the call's stream waits for the last copy
+        ck(cudaEventRecord(ctx->chunk_ev[ci % kMaxChunks], ctx->copy_stream), "copy event");
+        ck(cudaStreamWaitEvent(st, ctx->chunk_ev[ci % kMaxChunks], 0), "copy wait");
+        labels_copied = true;
+      }
     }
     ck(cudaGetLastError(), "kernel launch");
     if (host_io) {
-      ck(cudaMemcpyAsync(labels_out, lab, sizeof(int32_t) * nvs, cudaMemcpyDeviceToHost, st), "D2H labels");
-      if (dist)
-        ck(cudaMemcpyAsync(O.distances_out, dist, sizeof(double) * nvs, cudaMemcpyDeviceToHost, st),
-           "D2H distances");
+      if (!labels_copied) {
+        ck(cudaMemcpyAsync(labels_out, lab, sizeof(int32_t) * nvs, cudaMemcpyDeviceToHost, st), "D2H labels");
+        if (dist)
+          ck(cudaMemcpyAsync(O.distances_out, dist, sizeof(double) * nvs, cudaMemcpyDeviceToHost, st),
+             "D2H distances");
+      }
       if (hist)
         ck(cudaMemcpyAsync(O.histogram_out, hist, sizeof(unsigned long long) * ns,
                            cudaMemcpyDeviceToHost, st),
@@ -535,6 +570,8 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
               "VX_STATS gathered/CTA raw %.1f kept %.1f | brick list %.1f | sub-brick list %.2f "
               "(%llu CTAs, %llu bricks, %llu sub-bricks)\n",
               h[64] / nc, h[65] / nc, h[67] / nb, h[69] / ns2, h[66], h[68], h[70]);
+      fprintf(stderr, "VX_STATS max kept/CTA %llu, max brick list %llu, max sub-brick list %llu\n", h[71], h[72],
+              h[73]);
     }
     if (stats) tm.fill(stats->stage_ms);
     if (ctx->h_ctr->bad_site) return fail(VX_EINVAL, "site positions must lie strictly inside the domain");
@@ -545,7 +582,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       if (!use_brute) {
         stats->param = ctx->h_prm->param;
         stats->n_sites_kept = (int64_t)ctx->h_ctr->n_alive;
-        stats->n_unresolved = (int64_t)ctx->h_ctr->n_unres;
+        stats->n_unresolved = (int64_t)(ctx->h_ctr->n_unres + ctx->h_ctr->n_unres_done);
         stats->ball_evals = ctx->h_ctr->ball_evals;
         stats->shell_evals = ctx->h_ctr->shell_evals;
         stats->overflow_bricks = ctx->h_ctr->overflow_bricks;
@@ -601,6 +638,14 @@ void vx_context_destroy(vx_context* ctx) {
     if (ctx->h_prm) cudaFreeHost(ctx->h_prm);
     if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
     cudaStreamDestroy(ctx->stream);
+    if (ctx->copy_stream) {
+      cudaStreamSynchronize(ctx->copy_stream);
+      cudaStreamDestroy(ctx->copy_stream);
+      for (auto e : ctx->chunk_ev)
+        if (e) cudaEventDestroy(e);
+    }
+    for (auto e : ctx->ev)
+      if (e) cudaEventDestroy(e);
   }
   delete ctx;
 }

@@ -21,6 +21,12 @@ __global__ void init_kernel(DevParams* prm, DevCounters* ctr) {
   ctr->n_unres = ctr->ball_evals = ctr->shell_evals = ctr->overflow_bricks = 0;
   ctr->n_alive = 0;
   ctr->bad_site = 0;
+  ctr->n_unres_done = 0;
+}
+
+__global__ void chunk_roll_kernel(DevCounters* ctr) {
+  ctr->n_unres_done += ctr->n_unres;
+  ctr->n_unres = 0;
 }
 
 __global__ void voronoi_params_kernel(DevParams* prm, double R, double lmax) {
@@ -166,6 +172,11 @@ int launch_params(const Geo& g, const Bins& bins, DevParams* prm, const DevCount
 
 int launch_init(DevParams* prm, DevCounters* ctr, cudaStream_t st) {
   init_kernel<<<1, 1, 0, st>>>(prm, ctr);
+  return 1;
+}
+
+int launch_chunk_roll(DevCounters* ctr, cudaStream_t st) {
+  chunk_roll_kernel<<<1, 1, 0, st>>>(ctr);
   return 1;
 }
 

@@ -355,3 +355,40 @@ print("ok")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_chunked_host_copies_identical(kind):
+    """Host-buffer calls compute the slab in z-chunks and overlap each chunk's
+    D2H with the next chunk (VX_CHUNKS); labels, distances and histogram must
+    not depend on the chunking, and must match the oracle."""
+    import oracle
+    import paper_2201_13234_b200 as vx
+
+    rng = np.random.default_rng(900 + kind)
+    L = rng.uniform(0.5, 1.5, 3)
+    counts = [40, 36, 300]
+    ns = 300
+    G = 0.0 if kind == 0 else 0.7
+    pos, t = oracle.generate_uniform_sites(3, L, ns, kind, 1.0, 1234 + kind)
+    p = oracle.Problem(kind, counts, L, kind != 1, pos, t, G)
+    sites, grid = to_vx(p)
+    out = {}
+    old = os.environ.get("VX_CHUNKS")
+    try:
+        for ch in ("1", "5", "16"):
+            os.environ["VX_CHUNKS"] = ch
+            r = vx.tessellate_fast(sites, grid, vx.FastOptions(prune=True), distances=True, histogram=True)
+            out[ch] = r
+    finally:
+        if old is None:
+            os.environ.pop("VX_CHUNKS", None)
+        else:
+            os.environ["VX_CHUNKS"] = old
+    lab, dist = oracle.brute(p)
+    for ch, r in out.items():
+        assert np.array_equal(r.labels.labels, lab), ch
+        assert np.array_equal(r.distances.values.view(np.uint64), dist.view(np.uint64)), ch
+        assert np.array_equal(r.histogram, out["1"].histogram), ch
+    assert int(out["1"].histogram.sum()) == int(np.prod(counts))
