@@ -42,6 +42,7 @@ enum vx_status {
   VX_ECUDA = 2,        /* CUDA runtime / launch failure */
   VX_ENOMEM = 3,       /* device allocation failed */
   VX_EUNSUPPORTED = 4, /* outside this engine's domain (e.g. N_s >= 2^31) */
+  VX_EIO = 5,          /* reference: std::runtime_error from image I/O */
 };
 
 /* SiteSet + VoxelGrid of the reference (sites.hpp:15-31, geometry.hpp:27-78). */
@@ -159,6 +160,40 @@ int vx_generate_uniform_sites(int dim, const double* lengths, int64_t n_sites, i
 void vx_slab_bounds(int64_t n_last, int rank, int world, int64_t* begin_out, int64_t* end_out);
 /* FNV-style label fingerprint: h ^= label; h *= 1099511628211 */
 uint64_t vx_label_fingerprint(const int32_t* labels, int64_t n);
+
+/* ---- on-disk images (row f2; reference include/voxellate/image_io.hpp:17-29) ----
+ * Payload: raw little-endian labels (u32) or distances (f64), axis 0 fastest;
+ * sidecar `<path>.json`: format_version, type, d, dims, lengths, boundary,
+ * kind, n_sites, seed, payload_bytes.  type: 0 = "labels", 1 = "distances".
+ * Errors: VX_EIO (the reference's std::runtime_error) / VX_EINVAL, with the
+ * reference's message in vx_last_error(). */
+
+/* tessellate_fast + write_label_image (+ write_distance_image when
+ * distance_path != NULL) of the reference's run() (src/run.cpp:121-140,
+ * image_io.cpp:164-175): positions are host pointers; the image is computed in
+ * z-chunks and each chunk is copied out of device memory and appended to the
+ * file while later chunks are computed.  options->distances_out,
+ * histogram_out and device_pointers are ignored; seed goes to the sidecar
+ * (-1: sites not from a seeded generator). */
+int vx_tessellate_to_files(vx_context* ctx, const vx_problem* problem, const vx_options* options,
+                           const char* label_path, const char* distance_path, int64_t seed,
+                           vx_stats* stats);
+/* write_label_image / write_distance_image of a host image (image_io.cpp:164-175) */
+int vx_write_image(const char* path, int type, int dim, const int64_t* counts, const double* lengths,
+                   int periodic, int kind, int64_t n_sites, int64_t seed, const void* data);
+/* read_label_image / read_distance_image (image_io.cpp:177-202) with the
+ * reference's checks.  header_out[6] = {dim, periodic, kind, n_sites, seed,
+ * format_version}; counts_out / lengths_out hold VX_MAX_DIM entries; data may
+ * be NULL (header only) and is filled when cap_voxels >= the voxel count. */
+int vx_read_image(const char* path, int type, int64_t* header_out, int64_t* counts_out,
+                  double* lengths_out, void* data, int64_t cap_voxels);
+/* the sidecar alone: <path>.json, or its text into buf (returns its length) */
+int vx_write_image_sidecar(const char* path, const char* type, int dim, const int64_t* counts,
+                           const double* lengths, int periodic, int kind, int64_t n_sites,
+                           int64_t seed, uint64_t payload_bytes);
+int vx_image_sidecar_text(const char* type, int dim, const int64_t* counts, const double* lengths,
+                          int periodic, int kind, int64_t n_sites, int64_t seed,
+                          uint64_t payload_bytes, char* buf, int64_t cap);
 
 /* ---- measurement ---- */
 /* sustained f64 DADD and f32 FADD issue rates (adds/s) of `device`; the

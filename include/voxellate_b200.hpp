@@ -248,4 +248,75 @@ inline SiteSet generate_uniform_sites(const Domain& domain, std::int64_t n_sites
   return s;
 }
 
+// ---- on-disk images (row f2; reference include/voxellate/image_io.hpp) ----
+struct ImageMeta {  // image_io.hpp:13-19
+  int format_version = 1;
+  std::string type;
+  Kind kind = Kind::Voronoi;
+  std::int64_t n_sites = 0;
+  std::int64_t seed = -1;
+};
+
+namespace detail {
+inline void write_image(const std::string& path, int type, const VoxelGrid& g, const ImageMeta& meta,
+                        const void* data, std::size_t n) {
+  if ((std::int64_t)n != g.voxel_count()) throw std::invalid_argument("image payload size disagrees with its grid");
+  detail::check(vx_write_image(path.c_str(), type, g.dim(), g.counts.data(), g.domain.lengths.data(),
+                               g.domain.periodic() ? 1 : 0, (int)meta.kind, meta.n_sites, meta.seed, data));
+}
+template <class T>
+inline VoxelGrid read_image(const std::string& path, int type, std::vector<T>& data, ImageMeta* meta) {
+  std::int64_t hdr[6], counts[kMaxDim];
+  double lengths[kMaxDim];
+  detail::check(vx_read_image(path.c_str(), type, hdr, counts, lengths, nullptr, 0));
+  const int d = (int)hdr[0];
+  VoxelGrid g(std::vector<std::int64_t>(counts, counts + d),
+              Domain(std::vector<double>(lengths, lengths + d), hdr[1] ? Boundary::Periodic : Boundary::NonPeriodic));
+  data.resize((std::size_t)g.voxel_count());
+  detail::check(vx_read_image(path.c_str(), type, hdr, counts, lengths, data.data(), g.voxel_count()));
+  if (meta) {
+    meta->format_version = (int)hdr[5];
+    meta->type = type == 0 ? "labels" : "distances";
+    meta->kind = (Kind)hdr[2];
+    meta->n_sites = hdr[3];
+    meta->seed = hdr[4];
+  }
+  return g;
+}
+}  // namespace detail
+
+inline void write_label_image(const std::string& path, const LabelImage& image, const ImageMeta& meta) {
+  detail::write_image(path, 0, image.grid, meta, image.labels.data(), image.labels.size());
+}
+inline void write_distance_image(const std::string& path, const DistanceImage& image, const ImageMeta& meta) {
+  detail::write_image(path, 1, image.grid, meta, image.values.data(), image.values.size());
+}
+inline LabelImage read_label_image(const std::string& path, ImageMeta* meta = nullptr) {
+  LabelImage im;
+  im.grid = detail::read_image(path, 0, im.labels, meta);
+  return im;
+}
+inline DistanceImage read_distance_image(const std::string& path, ImageMeta* meta = nullptr) {
+  DistanceImage im;
+  im.grid = detail::read_image(path, 1, im.values, meta);
+  return im;
+}
+// tessellate_fast straight to the reference's files, the image streamed out of
+// device memory chunk by chunk (run.cpp:121-150 computes, then writes)
+inline void tessellate_to_files(const SiteSet& sites, const VoxelGrid& grid, const std::string& label_path,
+                                const std::string* distance_path = nullptr,
+                                const FastOptions& options = FastOptions(), std::int64_t seed = -1) {
+  vx_problem P = detail::problem(sites, grid);
+  vx_options O;
+  vx_options_init(&O);
+  O.prune = options.prune ? 1 : 0;
+  if (options.override_param) {
+    O.has_override = 1;
+    O.override_param = *options.override_param;
+  }
+  vx_stats st;
+  detail::check(vx_tessellate_to_files(nullptr, &P, &O, label_path.c_str(),
+                                       distance_path ? distance_path->c_str() : nullptr, seed, &st));
+}
+
 }  // namespace vxb200

@@ -97,6 +97,11 @@ def ref():
         L.vxref_slab_sample.argtypes = [C.c_int, C.c_int, C.c_int, _P, _P, _I64, _P, _P, _D,
                                         _I64, _I64, C.c_int, _P, _P]
         L.vxref_max_threads.restype = C.c_int
+        L.vxref_have_image_io.restype = C.c_int
+        if L.vxref_have_image_io():
+            L.vxref_write_image.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, _P, _P, C.c_int, _I64,
+                                            _I64, _P]
+            L.vxref_read_image.argtypes = [C.c_char_p, C.c_int, _P, _P, _P, _P, _I64]
         _ref = L
     return _ref
 
@@ -237,6 +242,40 @@ def ref_slab_sample(p: Problem, z0, z1, threads=0):
     if rc:
         raise RuntimeError(ref().vxref_last_error().decode())
     return lab, float(param[0])
+
+
+def ref_have_image_io() -> bool:
+    return have_ref() and bool(ref().vxref_have_image_io())
+
+
+def ref_write_image(path, type_, counts, lengths, periodic, kind, n_sites, seed, data):
+    """The reference's write_label_image / write_distance_image (image_io.cpp:164-175)."""
+    counts = np.ascontiguousarray(counts, dtype=np.int64)
+    lengths = np.ascontiguousarray(lengths, dtype=np.float64)
+    data = np.ascontiguousarray(data, dtype=np.uint32 if type_ == 0 else np.float64)
+    rc = ref().vxref_write_image(str(path).encode(), type_, counts.size, int(periodic), _ptr(counts),
+                                 _ptr(lengths), int(kind), int(n_sites), int(seed), _ptr(data))
+    if rc:
+        raise RuntimeError(ref().vxref_last_error().decode())
+
+
+def ref_read_image(path, type_):
+    """The reference's read_label_image / read_distance_image; returns
+    (header dict, data) or raises RuntimeError with the reference's message."""
+    hdr = np.zeros(6, dtype=np.int64)
+    dims = np.zeros(16, dtype=np.int64)
+    lengths = np.zeros(16, dtype=np.float64)
+    rc = ref().vxref_read_image(str(path).encode(), type_, _ptr(hdr), _ptr(dims), _ptr(lengths), None, 0)
+    if rc:
+        raise RuntimeError(ref().vxref_last_error().decode())
+    d = int(hdr[0])
+    nv = int(np.prod(dims[:d]))
+    data = np.empty(nv, dtype=np.uint32 if type_ == 0 else np.float64)
+    rc = ref().vxref_read_image(str(path).encode(), type_, _ptr(hdr), _ptr(dims), _ptr(lengths), _ptr(data), nv)
+    if rc:
+        raise RuntimeError(ref().vxref_last_error().decode())
+    return {"dim": d, "periodic": int(hdr[1]), "kind": int(hdr[2]), "n_sites": int(hdr[3]), "seed": int(hdr[4]),
+            "format_version": int(hdr[5]), "counts": dims[:d].tolist(), "lengths": lengths[:d].tolist()}, data
 
 
 # ---- BASELINE.json configs, SURVEY.md App. C recipe ----------------------

@@ -11,6 +11,9 @@
 //   optimal_v0 / radius_from_volume      include/voxellate/cost.hpp:13,28
 //   search_optimal_t0                    include/voxellate/cost.hpp:51
 //   validate_partition                   include/voxellate/tessellate.hpp:81-84
+//   write/read_label_image, write/read_distance_image
+//                                        include/voxellate/image_io.hpp:24-29
+//                                        (only when built with VXREF_IMAGE_IO)
 // vxref_slab_sample() re-drives the reference's own step-1 window scan
 // (detail::for_each_window_voxel, ball_scan.hpp:55-124) and step-2 full scan
 // for one z-slab, with the reference's param choice, so that bench.py can
@@ -29,6 +32,9 @@
 #include "voxellate/geometry.hpp"
 #include "voxellate/sites.hpp"
 #include "voxellate/tessellate.hpp"
+#ifdef VXREF_IMAGE_IO
+#include "voxellate/image_io.hpp"
+#endif
 
 using namespace voxellate;
 
@@ -312,5 +318,72 @@ int vxref_slab_sample(int kind, int dim, int periodic, const int64_t* counts,
       labels_out[i] = kept.empty() ? lab[i] : static_cast<uint32_t>(kept[lab[i]]);
   });
 }
+
+#ifdef VXREF_IMAGE_IO
+int vxref_have_image_io(void) { return 1; }
+
+// type 0: labels (u32 payload), 1: distances (f64 payload)
+int vxref_write_image(const char* path, int type, int dim, int periodic, const int64_t* counts,
+                      const double* lengths, int kind, int64_t n_sites, int64_t seed,
+                      const void* data) {
+  return guarded([&] {
+    ImageMeta meta;
+    meta.kind = static_cast<Kind>(kind);
+    meta.n_sites = n_sites;
+    meta.seed = seed;
+    const VoxelGrid grid = make_grid(dim, periodic, counts, lengths);
+    const int64_t nv = grid.voxel_count();
+    if (type == 0) {
+      LabelImage im;
+      im.grid = grid;
+      const auto* u = static_cast<const std::uint32_t*>(data);
+      im.labels.assign(u, u + nv);
+      write_label_image(path, im, meta);
+    } else {
+      DistanceImage im;
+      im.grid = grid;
+      const auto* v = static_cast<const double*>(data);
+      im.values.assign(v, v + nv);
+      write_distance_image(path, im, meta);
+    }
+  });
+}
+
+// header_out: [dim, periodic, kind, n_sites, seed, format_version], dims_out /
+// lengths_out: dim entries each (cap 16); data_out: voxel_count elements
+int vxref_read_image(const char* path, int type, int64_t* header_out, int64_t* dims_out,
+                     double* lengths_out, void* data_out, int64_t cap_voxels) {
+  return guarded([&] {
+    ImageMeta meta;
+    const VoxelGrid* g = nullptr;
+    LabelImage li;
+    DistanceImage di;
+    if (type == 0) {
+      li = read_label_image(path, &meta);
+      g = &li.grid;
+    } else {
+      di = read_distance_image(path, &meta);
+      g = &di.grid;
+    }
+    header_out[0] = g->dim();
+    header_out[1] = g->domain.boundary == Boundary::Periodic;
+    header_out[2] = static_cast<int64_t>(meta.kind);
+    header_out[3] = meta.n_sites;
+    header_out[4] = meta.seed;
+    header_out[5] = meta.format_version;
+    for (int i = 0; i < g->dim() && i < 16; ++i) {
+      dims_out[i] = g->counts[i];
+      lengths_out[i] = g->domain.lengths[i];
+    }
+    const int64_t nv = g->voxel_count();
+    if (data_out && nv <= cap_voxels) {
+      if (type == 0) std::memcpy(data_out, li.labels.data(), sizeof(std::uint32_t) * nv);
+      else std::memcpy(data_out, di.values.data(), sizeof(double) * nv);
+    }
+  });
+}
+#else
+int vxref_have_image_io(void) { return 0; }
+#endif
 
 }  // extern "C"

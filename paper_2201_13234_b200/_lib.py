@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libvoxellate_b200_debug.so" if os.environ.get("VX_LIB") == "debug" else "libvoxellate_b200.so")
 
-VX_OK, VX_EINVAL, VX_ECUDA, VX_ENOMEM, VX_EUNSUPPORTED = 0, 1, 2, 3, 4
+VX_OK, VX_EINVAL, VX_ECUDA, VX_ENOMEM, VX_EUNSUPPORTED, VX_EIO = 0, 1, 2, 3, 4, 5
 VX_MAX_DIM = 16
 
 
@@ -108,6 +108,15 @@ SIGNATURES = {
                               C.POINTER(C.c_int64)]),
     "vx_label_fingerprint": (C.c_uint64, [_P, C.c_int64]),
     "vx_probe_pipe_rates": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "vx_tessellate_to_files": (C.c_int, [_P, C.POINTER(vx_problem), C.POINTER(vx_options), C.c_char_p,
+                                         C.c_char_p, C.c_int64, C.POINTER(vx_stats)]),
+    "vx_write_image": (C.c_int, [C.c_char_p, C.c_int, C.c_int, _P, _P, C.c_int, C.c_int, C.c_int64,
+                                 C.c_int64, _P]),
+    "vx_read_image": (C.c_int, [C.c_char_p, C.c_int, _P, _P, _P, _P, C.c_int64]),
+    "vx_write_image_sidecar": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int, _P, _P, C.c_int, C.c_int,
+                                         C.c_int64, C.c_int64, C.c_uint64]),
+    "vx_image_sidecar_text": (C.c_int, [C.c_char_p, C.c_int, _P, _P, C.c_int, C.c_int, C.c_int64,
+                                        C.c_int64, C.c_uint64, C.c_char_p, C.c_int64]),
 }
 
 _lib = None

@@ -11,7 +11,9 @@
 // output semantics (labels = original site indices after prune, Voronoi
 // distances = sqrt of the best squared distance, tessellate.cpp:160-164,272-280).
 #include <cuda_runtime.h>
+#include <unistd.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -36,6 +38,12 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+}  // namespace
+
+void vxb::set_last_error(const std::string& msg) { g_err = msg; }
+
+namespace {
+
 struct Buf {
   void* p = nullptr;
   size_t n = 0;
@@ -57,6 +65,10 @@ struct vx_context {
   cudaEvent_t ev[8] = {};  // stage markers (options.profile_stages)
   cudaStream_t copy_stream = nullptr;  // chunked D2H of host-buffer calls
   cudaEvent_t chunk_ev[16] = {};
+  std::vector<cudaEvent_t> sink_ev;    // vx_tessellate_to_files: one per chunk
+  cudaEvent_t done_ev[2] = {};
+  void* pin[2] = {};                   // pinned double buffer of the file writer
+  size_t pin_bytes = 0;
 
   Buf* all[30] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
                   &vals_a,  &vals_b,  &bx,    &by,    &bz,     &bt,      &bidx,     &cell_start,
@@ -316,14 +328,130 @@ vx_context* resolve_context(vx_context* ctx, const vx_options* O, int* rc) {
   return c;
 }
 
+// bytes per streamed piece of vx_tessellate_to_files (VX_SINK_CHUNK_BYTES overrides, for tests)
+int64_t sink_chunk_bytes() {
+  const char* e = std::getenv("VX_SINK_CHUNK_BYTES");
+  return e ? std::max<int64_t>(4096, std::atoll(e)) : (256ll << 20);
+}
+
+struct SinkChunk {
+  int64_t z0, z1;
+  cudaEvent_t ev;  // recorded on the call's stream once the chunk is labelled
+};
+
+cudaEvent_t sink_event(vx_context* ctx, size_t i, cudaStream_t st) {
+  while (ctx->sink_ev.size() <= i) {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    ctx->sink_ev.push_back(e);
+  }
+  ck(cudaEventRecord(ctx->sink_ev[i], st), "chunk event");
+  return ctx->sink_ev[i];
+}
+
+struct FileSink;
+int write_sink(vx_context* ctx, const vx_problem* P, const FileSink& sink, const std::vector<SinkChunk>& chunks,
+               const int32_t* lab, const double* dist, int64_t zb, int64_t plane);
+
+// vx_tessellate_to_files: where the streamed image goes
+struct FileSink {
+  const char* lab_path;
+  const char* dist_path;  // NULL: labels only
+  int64_t seed;
+};
+
+// Double-buffered device -> pinned -> file streaming of the labelled chunks:
+// the copy of piece i+1 overlaps the file write of piece i, and every piece
+// waits only for the chunk that produced it (later chunks keep computing).
+int write_sink(vx_context* ctx, const vx_problem* P, const FileSink& sink, const std::vector<SinkChunk>& chunks,
+               const int32_t* lab, const double* dist, int64_t zb, int64_t plane) {
+  struct Piece {
+    int64_t z0, z1;
+    cudaEvent_t ev;
+    int which;  // 0 labels, 1 distances
+  };
+  std::vector<Piece> pieces;
+  size_t max_bytes = 0;
+  for (const SinkChunk& c : chunks) {
+    const int64_t step = std::max<int64_t>(1, sink_chunk_bytes() / (plane * (dist ? 8 : 4)));
+    for (int64_t a = c.z0; a < c.z1; a += step) {
+      const int64_t b = std::min(c.z1, a + step);
+      pieces.push_back({a, b, c.ev, 0});
+      if (dist) pieces.push_back({a, b, c.ev, 1});
+      max_bytes = std::max(max_bytes, (size_t)((b - a) * plane * (dist ? 8 : 4)));
+    }
+  }
+  if (!ctx->copy_stream) {
+    ck(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
+    for (auto& e : ctx->chunk_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  }
+  for (auto& e : ctx->done_ev)
+    if (!e) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  if (ctx->pin_bytes < max_bytes) {
+    for (auto& b : ctx->pin)
+      if (b) {
+        cudaFreeHost(b);
+        b = nullptr;
+      }
+    ctx->pin_bytes = 0;
+    for (auto& b : ctx->pin) ck(cudaMallocHost(&b, max_bytes), "pinned staging buffer");
+    ctx->pin_bytes = max_bytes;
+  }
+  int f[2] = {-1, -1};
+  int64_t off[2] = {0, 0};
+  const char* path[2] = {sink.lab_path, sink.dist_path};
+  int rc = io_open_payload(path[0], &f[0]);
+  if (!rc && dist) rc = io_open_payload(path[1], &f[1]);
+  auto issue = [&](size_t i) {
+    const Piece& q = pieces[i];
+    const size_t el = q.which ? 8 : 4;
+    const char* src = q.which ? reinterpret_cast<const char*>(dist) : reinterpret_cast<const char*>(lab);
+    ck(cudaStreamWaitEvent(ctx->copy_stream, q.ev, 0), "chunk wait");
+    ck(cudaMemcpyAsync(ctx->pin[i & 1], src + (size_t)(q.z0 - zb) * plane * el, (size_t)(q.z1 - q.z0) * plane * el,
+                       cudaMemcpyDeviceToHost, ctx->copy_stream),
+       "D2H image chunk");
+    ck(cudaEventRecord(ctx->done_ev[i & 1], ctx->copy_stream), "copy event");
+  };
+  try {
+    if (!rc && !pieces.empty()) issue(0);
+    for (size_t i = 0; !rc && i < pieces.size(); ++i) {
+      ck(cudaEventSynchronize(ctx->done_ev[i & 1]), "D2H image chunk");
+      if (i + 1 < pieces.size()) issue(i + 1);  // into the other buffer, already written out
+      const Piece& q = pieces[i];
+      const size_t nb = (size_t)(q.z1 - q.z0) * plane * (q.which ? 8 : 4);
+      rc = io_write_payload_at(f[q.which], path[q.which], ctx->pin[i & 1], nb, off[q.which]);
+      off[q.which] += (int64_t)nb;
+    }
+  } catch (...) {
+    for (int x : f)
+      if (x >= 0) ::close(x);
+    cudaStreamSynchronize(ctx->copy_stream);
+    throw;
+  }
+  cudaStreamSynchronize(ctx->copy_stream);
+  for (int k = 0; k < 2; ++k)
+    if (f[k] >= 0) {
+      const int rc2 = io_close_payload(f[k], path[k]);
+      if (!rc) rc = rc2;
+    }
+  if (rc) return rc;
+  const int64_t nv_total = plane * (P->counts[P->dim - 1]);
+  rc = vx_write_image_sidecar(sink.lab_path, "labels", P->dim, P->counts, P->lengths, P->periodic, P->kind,
+                              P->n_sites, sink.seed, (uint64_t)nv_total * 4u);
+  if (!rc && dist)
+    rc = vx_write_image_sidecar(sink.dist_path, "distances", P->dim, P->counts, P->lengths, P->periodic, P->kind,
+                                P->n_sites, sink.seed, (uint64_t)nv_total * 8u);
+  return rc;
+}
+
 int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t* labels_out,
-        vx_stats* stats, bool brute_engine) {
+        vx_stats* stats, bool brute_engine, const FileSink* sink = nullptr) {
   vx_options O;
   if (O_in) O = *O_in;
   else vx_options_init(&O);
   int rc = check_problem(P);
   if (rc) return rc;
-  if (!labels_out) return fail(VX_EINVAL, "labels_out must not be NULL");
+  if (!labels_out && !sink) return fail(VX_EINVAL, "labels_out must not be NULL");
   const int d = P->dim;
   const int64_t n_last = P->counts[d - 1];
   int64_t zb = O.slab_begin, ze = O.slab_end;
@@ -365,6 +493,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
   const int64_t ns = P->n_sites;
   StageTimer tm;
   bool labels_copied = false;  // chunked D2H already issued
+  std::vector<SinkChunk> sink_chunks;
   try {
     tm.on = O.profile_stages && !O.asynchronous;
     tm.st = st;
@@ -392,7 +521,8 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
     fill_geo(g, P, zb, ze, ns);
     int32_t* lab = host_io ? ensure<int32_t>(ctx->labels, (size_t)nvs) : labels_out;
     double* dist = nullptr;
-    if (O.distances_out) dist = host_io ? ensure<double>(ctx->dist, (size_t)nvs) : O.distances_out;
+    const bool want_dist = sink ? sink->dist_path != nullptr : O.distances_out != nullptr;
+    if (want_dist) dist = host_io ? ensure<double>(ctx->dist, (size_t)nvs) : O.distances_out;
     unsigned long long* hist = nullptr;
     if (O.histogram_out) {
       hist = host_io ? ensure<unsigned long long>(ctx->hist, (size_t)ns)
@@ -426,6 +556,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
                                lab, dist, hist, st);
       tm.mark(4);
       tm.mark(5);
+      if (sink) sink_chunks.push_back({zb, ze, sink_event(ctx, 0, st)});
     } else {
       Bins bins;
       double* bx = ensure<double>(ctx->bx, (size_t)ns);
@@ -496,11 +627,16 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       // call).  Chunks are whole super-bricks of the ball kernel (64 planes).
       const int64_t nz = ze - zb;
       int nchunk = 1;
-      if (host_io && !tm.on) {
+      if (host_io && !tm.on && !sink) {
         const char* e = std::getenv("VX_CHUNKS");
         nchunk = e ? std::max(1, std::min(kMaxChunks, std::atoi(e))) : (nz >= 256 ? 8 : 1);
       }
-      const int64_t cz = nchunk > 1 ? ((nz + nchunk - 1) / nchunk + 63) / 64 * 64 : nz;
+      int64_t cz = nchunk > 1 ? ((nz + nchunk - 1) / nchunk + 63) / 64 * 64 : nz;
+      if (sink) {  // file output: chunks of <= sink_chunk_bytes() per array, whole super-bricks
+        cz = std::max<int64_t>(1, sink_chunk_bytes() / (plane * (dist ? 8 : 4)));
+        if (cz >= 64) cz = cz / 64 * 64;
+        cz = std::min<int64_t>(cz, nz);
+      }
       if (nchunk > 1 && !ctx->copy_stream) {
         ck(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
         for (auto& e : ctx->chunk_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -517,6 +653,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
         gc.vec_store = (gc.n[0] % 4 == 0) && ((reinterpret_cast<uintptr_t>(lb) & 15) == 0);
         if (ci > 0) launches += launch_chunk_roll(ctr, st);
         ball_and_shell(gc, lb, ds);
+        if (sink) sink_chunks.push_back({c0, c1, sink_event(ctx, ci, st)});
         if (nchunk > 1) {
           cudaEvent_t ev = ctx->chunk_ev[ci % kMaxChunks];
           ck(cudaEventRecord(ev, st), "chunk event");
@@ -537,7 +674,12 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       }
     }
     ck(cudaGetLastError(), "kernel launch");
-    if (host_io) {
+    if (sink) {
+      rc = write_sink(ctx, P, *sink, sink_chunks, lab, dist, zb, plane);
+      if (rc) return rc;
+      labels_copied = true;
+    }
+    if (host_io && !sink) {
       if (!labels_copied) {
         ck(cudaMemcpyAsync(labels_out, lab, sizeof(int32_t) * nvs, cudaMemcpyDeviceToHost, st), "D2H labels");
         if (dist)
@@ -644,6 +786,11 @@ void vx_context_destroy(vx_context* ctx) {
       for (auto e : ctx->chunk_ev)
         if (e) cudaEventDestroy(e);
     }
+    for (auto e : ctx->sink_ev) cudaEventDestroy(e);
+    for (auto e : ctx->done_ev)
+      if (e) cudaEventDestroy(e);
+    for (auto b : ctx->pin)
+      if (b) cudaFreeHost(b);
     for (auto e : ctx->ev)
       if (e) cudaEventDestroy(e);
   }
@@ -665,6 +812,23 @@ int vx_tessellate(vx_context* ctx, const vx_problem* problem, const vx_options* 
 int vx_tessellate_brute(vx_context* ctx, const vx_problem* problem, const vx_options* options,
                         int32_t* labels_out, vx_stats* stats_out) {
   return run(ctx, problem, options, labels_out, stats_out, true);
+}
+
+int vx_tessellate_to_files(vx_context* ctx, const vx_problem* problem, const vx_options* options,
+                           const char* label_path, const char* distance_path, int64_t seed,
+                           vx_stats* stats) {
+  if (!label_path) return fail(VX_EINVAL, "label_path must not be NULL");
+  vx_options o;
+  if (options) o = *options;
+  else vx_options_init(&o);
+  o.device_pointers = 0;  // positions are host pointers; the image goes to the files
+  o.asynchronous = 0;
+  o.distances_out = nullptr;
+  o.histogram_out = nullptr;
+  o.slab_begin = o.slab_end = 0;  // the files hold the whole image
+  o.profile_stages = 0;
+  const FileSink sink{label_path, distance_path, seed};
+  return run(ctx, problem, &o, nullptr, stats, false, &sink);
 }
 
 int vx_prune(vx_context* ctx_in, const vx_problem* P, uint8_t* dropped_out, int64_t* n_removed) {

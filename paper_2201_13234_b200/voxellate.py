@@ -29,7 +29,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import check, lib, stats_dict, vx_options, vx_problem, vx_stats, vx_validation
+from ._lib import VX_MAX_DIM, check, lib, stats_dict, vx_options, vx_problem, vx_stats, vx_validation
 
 
 class Boundary(enum.Enum):
@@ -368,3 +368,95 @@ def slab_bounds(n_last: int, rank: int, world: int):
     b, e = C.c_int64(0), C.c_int64(0)
     lib().vx_slab_bounds(int(n_last), int(rank), int(world), C.byref(b), C.byref(e))
     return b.value, e.value
+
+
+# ---- on-disk images (row f2; reference include/voxellate/image_io.hpp:17-29) ----
+
+@dataclass
+class ImageMeta:
+    """image_io.hpp:13-19"""
+
+    format_version: int = 1
+    type: str = ""
+    kind: Kind = Kind.Voronoi
+    n_sites: int = 0
+    seed: int = -1
+
+
+def _grid_arrays(grid: VoxelGrid):
+    counts = np.ascontiguousarray(grid.counts, dtype=np.int64)
+    lengths = np.ascontiguousarray(grid.domain.lengths, dtype=np.float64)
+    return counts, lengths
+
+
+def _write_image(path: str, image, meta: ImageMeta, type_: int, data: np.ndarray) -> None:
+    counts, lengths = _grid_arrays(image.grid)
+    data = np.ascontiguousarray(data)
+    if data.size != image.grid.voxel_count():
+        raise ValueError("image payload size disagrees with its grid")
+    check(lib().vx_write_image(str(path).encode(), type_, image.grid.dim(), _ptr(counts), _ptr(lengths),
+                               1 if image.grid.domain.periodic() else 0, int(meta.kind), int(meta.n_sites),
+                               int(meta.seed), _ptr(data)))
+
+
+def write_label_image(path: str, image: LabelImage, meta: ImageMeta) -> None:
+    """Raw little-endian u32 labels, axis 0 fastest, + ``<path>.json`` (image_io.cpp:164-168)."""
+    _write_image(path, image, meta, 0, np.asarray(image.labels).view(np.uint32))
+
+
+def write_distance_image(path: str, image: DistanceImage, meta: ImageMeta) -> None:
+    """Raw little-endian f64 values + ``<path>.json`` (image_io.cpp:170-175)."""
+    _write_image(path, image, meta, 1, np.asarray(image.values, dtype=np.float64))
+
+
+def _read_image(path: str, type_: int):
+    hdr = np.zeros(6, dtype=np.int64)
+    counts = np.zeros(VX_MAX_DIM, dtype=np.int64)
+    lengths = np.zeros(VX_MAX_DIM, dtype=np.float64)
+    check(lib().vx_read_image(str(path).encode(), type_, _ptr(hdr), _ptr(counts), _ptr(lengths), None, 0))
+    d = int(hdr[0])
+    grid = VoxelGrid([int(c) for c in counts[:d]],
+                     Domain([float(x) for x in lengths[:d]],
+                            Boundary.Periodic if hdr[1] else Boundary.NonPeriodic))
+    data = np.empty(grid.voxel_count(), dtype=np.uint32 if type_ == 0 else np.float64)
+    check(lib().vx_read_image(str(path).encode(), type_, _ptr(hdr), _ptr(counts), _ptr(lengths), _ptr(data),
+                              data.size))
+    meta = ImageMeta(int(hdr[5]), "labels" if type_ == 0 else "distances", Kind(int(hdr[2])), int(hdr[3]),
+                     int(hdr[4]))
+    return grid, data, meta
+
+
+def read_label_image(path: str):
+    """(LabelImage, ImageMeta) with the reference's sidecar/payload checks (image_io.cpp:177-189)."""
+    grid, data, meta = _read_image(path, 0)
+    return LabelImage(grid, data), meta
+
+
+def read_distance_image(path: str):
+    """(DistanceImage, ImageMeta), image_io.cpp:191-202."""
+    grid, data, meta = _read_image(path, 1)
+    return DistanceImage(grid, data), meta
+
+
+def tessellate_to_files(sites: SiteSet, grid: VoxelGrid, label_path: str, distance_path: Optional[str] = None,
+                        options: Optional[FastOptions] = None, *, seed: int = -1, device=None,
+                        context=None) -> dict:
+    """tessellate_fast + write_label_image (+ write_distance_image), as the
+    reference's run() does (run.cpp:121-150), streaming each z-chunk of the
+    image out of device memory into the files while later chunks compute.
+    Returns the call's stats."""
+    P = _problem(sites, grid)
+    O = vx_options()
+    lib().vx_options_init(C.byref(O))
+    options = options or FastOptions()
+    O.prune = 1 if options.prune else 0
+    if options.override_param is not None:
+        O.has_override = 1
+        O.override_param = float(options.override_param)
+    if device is not None:
+        O.device = int(device)
+    st = vx_stats()
+    check(lib().vx_tessellate_to_files(context, C.byref(P), C.byref(O), str(label_path).encode(),
+                                       None if distance_path is None else str(distance_path).encode(),
+                                       int(seed), C.byref(st)))
+    return stats_dict(st)

@@ -11,6 +11,9 @@
 
 #include "voxellate/sites.hpp"
 #include "voxellate/tessellate.hpp"
+#ifdef VXREF_IMAGE_IO
+#include "voxellate/image_io.hpp"
+#endif
 #include "voxellate_b200.hpp"
 
 namespace R = voxellate;
@@ -115,6 +118,64 @@ int main() {
             a.value_mismatches == b.value_mismatches && a.examples == b.examples);
     }
   }
+#ifdef VXREF_IMAGE_IO
+  // on-disk images: the shim writes, the reference reads (and the other way);
+  // payload and sidecar bytes are identical
+  {
+    R::Domain rbox({1.5, 0.75, 2.0}, R::Boundary::NonPeriodic);
+    R::VoxelGrid rgrid({5, 4, 3}, rbox);
+    R::SiteSet rs = R::generate_uniform_sites(rbox, 9, R::Kind::JohnsonMehl, 0.8, 1.0, 5);
+    R::TessResult rr = R::tessellate_fast(rs, rgrid);
+    G::Domain gbox({1.5, 0.75, 2.0}, G::Boundary::NonPeriodic);
+    G::VoxelGrid ggrid({5, 4, 3}, gbox);
+    G::SiteSet gs = G::generate_uniform_sites(gbox, 9, G::Kind::JohnsonMehl, 0.8, 1.0, 5);
+    G::TessResult gr = G::tessellate_fast(gs, ggrid);
+    R::ImageMeta rm;
+    rm.kind = R::Kind::JohnsonMehl;
+    rm.n_sites = 9;
+    rm.seed = 5;
+    G::ImageMeta gm;
+    gm.kind = G::Kind::JohnsonMehl;
+    gm.n_sites = 9;
+    gm.seed = 5;
+    R::write_label_image("/tmp/vx_shim_r.lab", rr.labels, rm);
+    R::write_distance_image("/tmp/vx_shim_r.dist", rr.distances, rm);
+    G::write_label_image("/tmp/vx_shim_g.lab", gr.labels, gm);
+    G::write_distance_image("/tmp/vx_shim_g.dist", gr.distances, gm);
+    auto slurp = [](const char* p) {
+      std::string out;
+      if (FILE* f = std::fopen(p, "rb")) {
+        char b[4096];
+        size_t n;
+        while ((n = std::fread(b, 1, sizeof(b), f)) > 0) out.append(b, n);
+        std::fclose(f);
+      }
+      return out;
+    };
+    for (const char* sfx : {".lab", ".lab.json", ".dist", ".dist.json"}) {
+      const std::string a = slurp((std::string("/tmp/vx_shim_r") + sfx).c_str());
+      const std::string b = slurp((std::string("/tmp/vx_shim_g") + sfx).c_str());
+      CHECK(!a.empty() && a == b);
+    }
+    R::ImageMeta m1;
+    const R::LabelImage back_r = R::read_label_image("/tmp/vx_shim_g.lab", &m1);
+    CHECK(back_r.labels == rr.labels.labels && m1.seed == 5 && m1.n_sites == 9);
+    G::ImageMeta m2;
+    const G::DistanceImage back_g = G::read_distance_image("/tmp/vx_shim_r.dist", &m2);
+    CHECK(std::memcmp(back_g.values.data(), rr.distances.values.data(), sizeof(double) * back_g.values.size()) == 0);
+    bool threw = false;
+    try {
+      G::read_distance_image("/tmp/vx_shim_r.lab");
+    } catch (const std::runtime_error& e) {
+      threw = std::string(e.what()) == "image /tmp/vx_shim_r.lab has type 'labels', expected 'distances'";
+    }
+    CHECK(threw);
+    for (const char* p : {"/tmp/vx_shim_r.lab", "/tmp/vx_shim_r.dist", "/tmp/vx_shim_g.lab", "/tmp/vx_shim_g.dist"}) {
+      std::remove(p);
+      std::remove((std::string(p) + ".json").c_str());
+    }
+  }
+#endif
   std::printf("%d instances, %d failures\n", instances, failures);
   if (failures == 0) std::printf("ALL OK\n");
   return failures == 0 ? 0 : 1;

@@ -392,3 +392,49 @@ def test_chunked_host_copies_identical(kind):
         assert np.array_equal(r.distances.values.view(np.uint64), dist.view(np.uint64)), ch
         assert np.array_equal(r.histogram, out["1"].histogram), ch
     assert int(out["1"].histogram.sum()) == int(np.prod(counts))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["vor3d", "jm3d_dist", "lag2d", "brute4d"])
+def test_tessellate_to_files_streams_the_image(case, tmp_path):
+    """vx_tessellate_to_files streams each z-chunk of the image from device
+    memory into the reference's file format (row f2); forced small pieces
+    (VX_SINK_CHUNK_BYTES) exercise the double-buffered copy/write pipeline."""
+    import json as _json
+
+    import oracle
+    import paper_2201_13234_b200 as vx
+
+    spec = {"vor3d": (0, [48, 40, 200], 400, False), "jm3d_dist": (1, [30, 33, 120], 200, True),
+            "lag2d": (2, [301, 257], 150, True), "brute4d": (0, [6, 5, 4, 30], 40, True)}[case]
+    kind, counts, ns, with_dist = spec
+    d = len(counts)
+    rng = np.random.default_rng(77)
+    L = rng.uniform(0.5, 1.5, d)
+    pos, t = oracle.generate_uniform_sites(d, L, ns, kind, 1.0, 4242)
+    p = oracle.Problem(kind, counts, L, kind != 1, pos, t, 0.0 if kind == 0 else 0.8)
+    sites, grid = to_vx(p)
+    lab_path = str(tmp_path / "img.lab")
+    dist_path = str(tmp_path / "img.dist") if with_dist else None
+    old = os.environ.get("VX_SINK_CHUNK_BYTES")
+    os.environ["VX_SINK_CHUNK_BYTES"] = "20000"
+    try:
+        vx.tessellate_to_files(sites, grid, lab_path, dist_path, seed=5)
+    finally:
+        if old is None:
+            os.environ.pop("VX_SINK_CHUNK_BYTES", None)
+        else:
+            os.environ["VX_SINK_CHUNK_BYTES"] = old
+    lab, dist = oracle.brute(p)
+    assert np.array_equal(np.fromfile(lab_path, dtype="<u4"), lab.astype(np.uint32))
+    side = _json.load(open(lab_path + ".json"))
+    assert side == {"format_version": 1, "type": "labels", "d": d, "dims": list(counts), "lengths": list(L),
+                    "boundary": "periodic" if kind != 1 else "non-periodic",
+                    "kind": ["voronoi", "johnson-mehl", "laguerre"][kind], "n_sites": ns, "seed": 5,
+                    "payload_bytes": 4 * int(np.prod(counts))}
+    im, meta = vx.read_label_image(lab_path)
+    assert np.array_equal(im.labels, lab.astype(np.uint32)) and meta.seed == 5
+    if with_dist:
+        assert np.array_equal(np.fromfile(dist_path, dtype="<f8").view(np.uint64), dist.view(np.uint64))
+        dim_, _ = vx.read_distance_image(dist_path)
+        assert np.array_equal(dim_.values.view(np.uint64), dist.view(np.uint64))
