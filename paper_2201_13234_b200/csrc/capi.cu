@@ -600,12 +600,13 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
                                 ball_scale, scratch, st);
       dbg(st, "params");
       tm.mark(3);
-      static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 10;
+      static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 11;
       static const int bzw = std::getenv("VX_BZW") ? std::atoi(std::getenv("VX_BZW")) : 4;
       static const int sy = std::getenv("VX_SY") ? std::atoi(std::getenv("VX_SY")) : 4;
       auto ball_and_shell = [&](const Geo& gg, int32_t* lb, double* ds) {
         unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
-        if (ball_ver == 10) launches += launch_ball10(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
+        if (ball_ver == 11) launches += launch_ball11(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
+        else if (ball_ver == 10) launches += launch_ball10(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
         else if (ball_ver == 9) launches += launch_ball9(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
         else if (ball_ver == 8) launches += launch_ball8(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
         else if (ball_ver == 7) launches += launch_ball7(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
