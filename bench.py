@@ -197,13 +197,16 @@ def run_ours(args):
     world, rank, local = dist_env()
     if world != args.gpus:
         args.gpus = world
-    dev = local
+    dev = 0 if args.same_gpu else local
     torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
     c, box, grid, sites = make_inputs(args.config)
     n = c["n"]
     zb, ze = vx.slab_bounds(n, rank, world)
@@ -327,7 +330,8 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: SURVEY.md App. C seeded uniform sites (mt19937_64, seed 1000+cfg)",
         "config": {"workload": c["name"], "n_voxels": nv_total, "n_sites": ns,
-                   "parallelism": f"z-slab x{world}" + (" + NCCL histogram all-reduce" if world > 1 else ""),
+                   "parallelism": f"z-slab x{world}" + (f" + {args.dist_backend.upper()} histogram all-reduce"
+                                                          if world > 1 else ""),
                    "l2": "flushed between steps (256 MB write); labels 4 B/voxel > L2",
                    "labels": "int32 in HBM", "histogram": "uint64 grain volumes"},
         "clocks": clk.summary(),
@@ -362,6 +366,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-planes", type=int, default=32)
     ap.add_argument("--ref-planes", type=int, default=32)
+    # functional dry run of the N > 1 path on a one-GPU box (not a measurement):
+    # gloo collectives, every rank on cuda:0
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"], help=argparse.SUPPRESS)
+    ap.add_argument("--same-gpu", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
