@@ -438,3 +438,37 @@ def test_tessellate_to_files_streams_the_image(case, tmp_path):
         assert np.array_equal(np.fromfile(dist_path, dtype="<f8").view(np.uint64), dist.view(np.uint64))
         dim_, _ = vx.read_distance_image(dist_path)
         assert np.array_equal(dim_.values.view(np.uint64), dist.view(np.uint64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("i", range(30))
+def test_large_random_vs_reference_library(i):
+    """Random problems at realistic size (3-D 96..200 voxels per axis, 2-D
+    600..1200, non-cubic, all kinds, both boundaries, prune on/off) against the reference library
+    itself (oracle/_ref, run on the box's host cores): labels, values and the
+    grain-volume histogram, bit for bit."""
+    import oracle
+    import paper_2201_13234_b200 as vx
+
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(31337 + i)
+    kind = i % 3
+    periodic = bool((i // 3) % 2 == 0)
+    d = 2 if i % 5 == 4 else 3
+    counts = [int(x) for x in rng.integers(96, 201, 3)] if d == 3 else [int(x) for x in rng.integers(600, 1201, 2)]
+    L = rng.uniform(0.5, 2.0, d)
+    sp = float(np.min(L / np.array(counts)))
+    spacing_vox = float(rng.uniform(4.0, 14.0))
+    ns = int(np.clip(np.prod(L) / (spacing_vox * sp) ** d, 50, 60000))
+    horizon = float(0.5 * np.prod(L) ** (1.0 / d) / ns ** (1.0 / d))
+    pos, t = oracle.generate_uniform_sites(d, L, ns, kind, horizon, 555 + i)
+    G = [0.0, float(rng.uniform(0.5, 2.0)), float(rng.uniform(0.5, 2.0))][kind]
+    p = oracle.Problem(kind, counts, L, periodic, pos, t, G)
+    prune = bool(i % 4 != 3)
+    lab_ref, dist_ref, _, _ = oracle.ref_tessellate(p, prune=prune)
+    sites, grid = to_vx(p)
+    r = vx.tessellate_fast(sites, grid, vx.FastOptions(prune=prune), distances=True, histogram=True)
+    assert np.array_equal(r.labels.labels, lab_ref), int((r.labels.labels != lab_ref).sum())
+    assert np.array_equal(r.distances.values.view(np.uint64), dist_ref.view(np.uint64))
+    assert np.array_equal(r.histogram, np.bincount(lab_ref, minlength=ns).astype(np.uint64))
