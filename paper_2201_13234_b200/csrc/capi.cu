@@ -353,11 +353,16 @@ struct FileSink;
 int write_sink(vx_context* ctx, const vx_problem* P, const FileSink& sink, const std::vector<SinkChunk>& chunks,
                const int32_t* lab, const double* dist, int64_t zb, int64_t plane);
 
-// vx_tessellate_to_files: where the streamed image goes
+// Where a streamed image goes: files (vx_tessellate_to_files) or, for a
+// host-buffer call whose output is pageable memory, the caller's buffers
+// (staged through pinned memory: the driver's own pageable copies run at a
+// few GB/s).
 struct FileSink {
   const char* lab_path;
   const char* dist_path;  // NULL: labels only
   int64_t seed;
+  char* mem[2] = {nullptr, nullptr};  // memory mode: labels, distances
+  bool to_memory() const { return mem[0] != nullptr; }
 };
 
 // Double-buffered device -> pinned -> file streaming of the labelled chunks:
@@ -400,8 +405,11 @@ int write_sink(vx_context* ctx, const vx_problem* P, const FileSink& sink, const
   int f[2] = {-1, -1};
   int64_t off[2] = {0, 0};
   const char* path[2] = {sink.lab_path, sink.dist_path};
-  int rc = io_open_payload(path[0], &f[0]);
-  if (!rc && dist) rc = io_open_payload(path[1], &f[1]);
+  int rc = VX_OK;
+  if (!sink.to_memory()) {
+    rc = io_open_payload(path[0], &f[0]);
+    if (!rc && dist) rc = io_open_payload(path[1], &f[1]);
+  }
   auto issue = [&](size_t i) {
     const Piece& q = pieces[i];
     const size_t el = q.which ? 8 : 4;
@@ -419,7 +427,8 @@ int write_sink(vx_context* ctx, const vx_problem* P, const FileSink& sink, const
       if (i + 1 < pieces.size()) issue(i + 1);  // into the other buffer, already written out
       const Piece& q = pieces[i];
       const size_t nb = (size_t)(q.z1 - q.z0) * plane * (q.which ? 8 : 4);
-      rc = io_write_payload_at(f[q.which], path[q.which], ctx->pin[i & 1], nb, off[q.which]);
+      if (sink.to_memory()) io_copy_parallel(sink.mem[q.which] + off[q.which], ctx->pin[i & 1], nb);
+      else rc = io_write_payload_at(f[q.which], path[q.which], ctx->pin[i & 1], nb, off[q.which]);
       off[q.which] += (int64_t)nb;
     }
   } catch (...) {
@@ -434,7 +443,7 @@ int write_sink(vx_context* ctx, const vx_problem* P, const FileSink& sink, const
       const int rc2 = io_close_payload(f[k], path[k]);
       if (!rc) rc = rc2;
     }
-  if (rc) return rc;
+  if (rc || sink.to_memory()) return rc;
   const int64_t nv_total = plane * (P->counts[P->dim - 1]);
   rc = vx_write_image_sidecar(sink.lab_path, "labels", P->dim, P->counts, P->lengths, P->periodic, P->kind,
                               P->n_sites, sink.seed, (uint64_t)nv_total * 4u);
@@ -442,6 +451,15 @@ int write_sink(vx_context* ctx, const vx_problem* P, const FileSink& sink, const
     rc = vx_write_image_sidecar(sink.dist_path, "distances", P->dim, P->counts, P->lengths, P->periodic, P->kind,
                                 P->n_sites, sink.seed, (uint64_t)nv_total * 8u);
   return rc;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
 }
 
 int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t* labels_out,
@@ -521,7 +539,14 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
     fill_geo(g, P, zb, ze, ns);
     int32_t* lab = host_io ? ensure<int32_t>(ctx->labels, (size_t)nvs) : labels_out;
     double* dist = nullptr;
-    const bool want_dist = sink ? sink->dist_path != nullptr : O.distances_out != nullptr;
+    // host-buffer call into pageable memory: stage through pinned buffers
+    FileSink mem_sink{nullptr, nullptr, -1};
+    if (host_io && !sink && !tm.on && (size_t)nvs * 4 >= (16u << 20) && !is_pinned(labels_out)) {
+      mem_sink.mem[0] = reinterpret_cast<char*>(labels_out);
+      mem_sink.mem[1] = reinterpret_cast<char*>(O.distances_out);
+      sink = &mem_sink;
+    }
+    const bool want_dist = sink ? (sink->dist_path != nullptr || sink->mem[1] != nullptr) : O.distances_out != nullptr;
     if (want_dist) dist = host_io ? ensure<double>(ctx->dist, (size_t)nvs) : O.distances_out;
     unsigned long long* hist = nullptr;
     if (O.histogram_out) {
@@ -680,7 +705,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       if (rc) return rc;
       labels_copied = true;
     }
-    if (host_io && !sink) {
+    if (host_io) {
       if (!labels_copied) {
         ck(cudaMemcpyAsync(labels_out, lab, sizeof(int32_t) * nvs, cudaMemcpyDeviceToHost, st), "D2H labels");
         if (dist)

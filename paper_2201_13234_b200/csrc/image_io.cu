@@ -354,6 +354,26 @@ int io_write_payload_at(int fd, const char* path, const void* data, size_t bytes
     if (!v) return io::io_fail(VX_EIO, std::string("failed writing image payload: ") + path);
   return VX_OK;
 }
+// pinned staging buffer -> caller's pageable memory, several threads (the
+// destination's first-touch page faults parallelise across threads)
+void io_copy_parallel(void* dst, const void* src, size_t bytes) {
+  const size_t kMinSlice = 4u << 20;
+  const int nt = (int)std::max<size_t>(1, std::min<size_t>(std::min(16u, std::max(1u, std::thread::hardware_concurrency())),
+                                                         bytes / kMinSlice));
+  auto work = [&](int t) {
+    const size_t a = bytes * t / nt, b = bytes * (t + 1) / nt;
+    std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+  };
+  if (nt == 1) {
+    work(0);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+}
+
 int io_close_payload(int fd, const char* path) {
   if (::close(fd) != 0) return io::io_fail(VX_EIO, std::string("failed writing image payload: ") + path);
   return VX_OK;
