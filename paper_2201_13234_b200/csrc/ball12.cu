@@ -1,0 +1,865 @@
+// K2 (v12): the ball phase of v11 split in two kernels.
+//
+//   cull12  : v11's gather, column tau/mask passes, brick lists and sub-brick
+//             tau + bisector culls; each 8x8x4 sub-brick's survivors (binned
+//             positions, in ascending site index) go to a global list, with
+//             (offset, count) per sub-brick (count -1: overflow, the eval
+//             kernel sends every voxel of it to the shell search).
+//   eval12  : one warp per sub-brick: the exact per-axis f64 tables, the exact
+//             evaluation of 8 voxels per lane, label / distance stores, the
+//             histogram counts and the unresolved compaction.
+// Each kernel needs fewer registers and much less shared memory than the
+// fused v11, so both run at higher occupancy; the lists cost ~9 ints per
+// sub-brick of HBM traffic.
+//
+// v11 (below, unchanged up to the sub-brick cull):
+//
+// v11 = v10 with the brick-level tau and list passes merged over the warp's
+// column of bricks: one pass computes the upper bounds of every gathered site
+// for all (up to 4) bricks of the column at once (the x/y terms are shared),
+// one pass the lower bounds and a per-site keep mask; each brick's list is then
+// a ballot over the mask bits in site-index order.  The column height (1, 2 or
+// 4 bricks) is chosen by the host from the site density so that the gathered
+// list fits kTcap.
+//
+// v10 = v8 with 8x8x4 sub-bricks (two per brick, 8 voxels per lane in two
+// y-rows that share the x tables) and the brick list sorted by site index once
+// per brick, so each sub-brick's ballot-compacted survivors are already in the
+// reference's ascending order.  Per-sub-brick overhead (cull, tables, store) is
+// spread over 256 voxels instead of 128.
+//
+// Same contract as ball.cu (see its header): labels/values bit-identical to
+// the reference because every culled site loses strictly, by far more than
+// f64 rounding, at every voxel of the box it was culled for, and the survivors
+// are evaluated with the reference's exact f64 fold in ascending site order.
+//
+// Work split (one CTA = 8 warps = a 16^3 "super-brick"):
+//   G (CTA)  : x-rows of cells within R of the super-brick -> gathered site
+//              list in shared memory (f32 coordinates relative to the super-
+//              brick centre + time, plus the binned index); one barrier.
+//   W (warp) : each warp owns an 8^3 brick: tau = min over gathered sites of
+//              an upper bound of prox over the brick; keep sites whose lower
+//              bound is <= tau  (f32, outward-rounded margins).
+//   S (warp) : for each of the brick's four 8x4x4 sub-bricks: the same tau
+//              cull on the brick list plus the bisector test against the
+//              sub-brick's tau site s0 -> a handful of survivors, sorted by
+//              site index, exact per-axis f64 tables (ball_scan.hpp:89-96),
+//              exact evaluation of 4 voxels per lane, resolve (prox <= cutoff),
+//              int4 label stores, warp-aggregated unresolved push and
+//              per-candidate histogram counts.
+// f32 bounds: every bound is widened by kRel (1e-5) relative to the magnitude
+// of its terms plus an absolute coordinate slack e_d; float rounding is ~1e-7
+// relative, so a site is only culled if it loses by >> f64 rounding.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "vx_internal.cuh"
+
+// VX_STATS=1 in the environment: per-level list sizes into eval_slots[64..70]
+#define VX_STATS_ON (g.stats_on != 0)
+
+namespace vxb {
+namespace v12 {
+
+constexpr int kSB = 16;           // super-brick edge along x and y (voxels)
+constexpr int kMaxBB = 4;         // bricks per warp column (super-brick z = 16 nbb <= 64)
+constexpr int kSZ = 16 * kMaxBB;
+constexpr int kB2Threads = 256;   // 8 warps, one 8^3 brick each
+constexpr int kTcap = 512;        // sites kept per super-brick (else the CTA falls back)
+constexpr int kWcap = 64;         // brick-level survivors per warp (2 slots per lane)
+constexpr int kFcap = 32;         // sub-brick survivors per warp (exact stage)
+constexpr int kRows2 = 256;       // cell rows per super-brick
+constexpr float kRel = 1e-5f;
+
+struct FBox {
+  float c[3];  // centre relative to the super-brick centre
+  float h[3];  // half extent (+ slack)
+};
+
+struct __align__(16) WarpSmem {
+  int W[kWcap];        // brick list (gather slots), ascending site index
+};
+
+// eval12: per warp (one sub-brick)
+struct __align__(16) EvalSmem {
+  double T[kFcap][20]; // exact w^2: [0,8) x, [8,16) y, [16,20) z
+  double Ft[kFcap];
+  int P[kFcap];        // binned positions
+  int Fidx[kFcap];
+  int cnt[kFcap];
+};
+
+struct Smem2 {
+  float4 rel[kTcap];   // (ux, uy, uz, t) relative to the super-brick centre
+  int p[kTcap];        // binned position
+  int idx[kTcap];      // original site index
+  unsigned char flag[kTcap];  // bit a: periodic image ambiguous on axis a
+  short ord[kTcap];    // gather slots in ascending site-index order
+  unsigned char mk[kB2Threads / 32][kTcap];  // per warp: bit b = kept for brick b of its column
+  int seg_start[2 * kRows2];
+  int seg_off[2 * kRows2 + 1];
+  int warp_tot[kB2Threads / 32];
+  int n_total;
+  int n_kept;
+  double cx[kSB], cy[kSB], cz[kSZ];  // exact voxel centres of the super-brick
+  WarpSmem w[kB2Threads / 32];
+};
+
+__device__ __forceinline__ float lo_add(float a, float b) {
+  return (a + b) - kRel * (fabsf(a) + fabsf(b));
+}
+__device__ __forceinline__ float hi_add(float a, float b) {
+  return (a + b) + kRel * (fabsf(a) + fabsf(b));
+}
+
+struct SiteF {
+  float v[3], mn[3], mx[3];
+  float t;
+  float lbp, ubp;
+  float lb, ub;  // squared distance bounds
+};
+
+// Conservative prox bounds of one gathered site over box B.
+template <int KIND, bool PER>
+__device__ __forceinline__ void fbounds(const float4 s, unsigned flags, const FBox& B,
+                                        const float* halfL, float invG, SiteF& o) {
+  const float u[3] = {s.x, s.y, s.z};
+  float lb = 0.f, ub = 0.f;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float va = u[a] - B.c[a];
+    const float av = fabsf(va);
+    float lo = fmaxf(av - B.h[a], 0.f), hi = av + B.h[a];
+    if (PER) {
+      if (flags & (1u << a)) {
+        lo = 0.f;
+        hi = halfL[a];
+      } else {
+        hi = fminf(hi, halfL[a]);
+      }
+    }
+    o.v[a] = va;
+    o.mn[a] = lo;
+    o.mx[a] = hi;
+    lb = __fmaf_rn(lo, lo, lb);
+    ub = __fmaf_rn(hi, hi, ub);
+  }
+  lb *= (1.f - kRel);
+  ub *= (1.f + kRel);
+  o.lb = lb;
+  o.ub = ub;
+  o.t = s.w;
+  if (KIND == kVoronoi) {
+    o.lbp = lb;
+    o.ubp = ub;
+  } else {
+    const float tl = s.w - kRel * fabsf(s.w), th = s.w + kRel * fabsf(s.w);
+    const float dl = KIND == kJohnsonMehl ? sqrtf(lb) : lb;
+    const float dh = KIND == kJohnsonMehl ? sqrtf(ub) : ub;
+    o.lbp = lo_add(dl * invG * (1.f - kRel), tl);
+    o.ubp = hi_add(dh * invG * (1.f + kRel), th);
+  }
+}
+
+// true iff s may beat (or tie) s0 somewhere in B: lower bound of prox_s - prox_s0 <= 0.
+template <int KIND, bool PER>
+__device__ __forceinline__ bool bisector_keep(const SiteF& s, unsigned fs, const SiteF& z,
+                                              unsigned f0, const FBox& B, const float* halfL,
+                                              float invG, float e_d) {
+  float D = 0.f, mag = 0.f;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const bool wrapcase = PER && (((fs | f0) >> a) & 1u ||
+                                  fabsf(s.v[a]) + B.h[a] > halfL[a] * (1.f - 1e-5f) ||
+                                  fabsf(z.v[a]) + B.h[a] > halfL[a] * (1.f - 1e-5f));
+    float term, m;
+    if (wrapcase) {
+      term = s.mn[a] * s.mn[a] - z.mx[a] * z.mx[a];
+      m = s.mn[a] * s.mn[a] + z.mx[a] * z.mx[a];
+    } else {
+      const float dv = fabsf(s.v[a] - z.v[a]);
+      term = s.v[a] * s.v[a] - z.v[a] * z.v[a] - 2.f * B.h[a] * dv;
+      m = s.v[a] * s.v[a] + z.v[a] * z.v[a] + 2.f * B.h[a] * dv;
+    }
+    D += term;
+    mag += m + 2.f * e_d * (fabsf(s.v[a]) + fabsf(z.v[a]) + 2.f * B.h[a] + e_d);
+  }
+  const float Dlo = D - kRel * mag;  // lower bound of min_B (d_s^2 - d_s0^2)
+  if (KIND == kVoronoi) return Dlo <= 0.f;
+  const float dt = lo_add(s.t - kRel * fabsf(s.t), -(z.t + kRel * fabsf(z.t)));
+  if (KIND == kLaguerre) {
+    const float q = Dlo >= 0.f ? Dlo * invG * (1.f - kRel) : Dlo * invG * (1.f + kRel);
+    return lo_add(q, dt) <= 0.f;
+  }
+  // JM: |x-s| - |x-s0| = N / (|x-s| + |x-s0|)
+  float q;
+  if (Dlo >= 0.f) {
+    const float dhi = (sqrtf(s.ub) + sqrtf(z.ub)) * (1.f + kRel);
+    q = Dlo / dhi * (1.f - kRel);
+  } else {
+    const float dlo = (sqrtf(s.lb) + sqrtf(z.lb)) * (1.f - kRel);
+    if (!(dlo > 0.f)) return true;
+    q = Dlo / dlo * (1.f + kRel);
+  }
+  q = q >= 0.f ? q * invG * (1.f - kRel) : q * invG * (1.f + kRel);
+  return lo_add(q, dt) <= 0.f;
+}
+
+__device__ __forceinline__ long long wrapi2(long long c, long long m) {
+  const long long r = c % m;
+  return r < 0 ? r + m : r;
+}
+
+template <int KIND, bool PER>
+__global__ void __launch_bounds__(kB2Threads, 4)
+    cull12_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, int2* __restrict__ info,
+                  int* __restrict__ list, long long list_cap, int* __restrict__ list_count,
+                  DevCounters* ctr, unsigned long long* __restrict__ eval_slots, int nbb) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem2& S = *reinterpret_cast<Smem2*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+  const long long K0[3] = {(long long)blockIdx.x * kSB, (long long)blockIdx.y * kSB,
+                           g.z_begin + (long long)blockIdx.z * (16 * nbb)};
+  int ext[3];
+  ext[0] = (int)min((long long)kSB, g.n[0] - K0[0]);
+  ext[1] = (int)min((long long)kSB, g.n[1] - K0[1]);
+  ext[2] = (int)min((long long)(16 * nbb), g.z_end - K0[2]);
+  double blo[3], bhi[3], cc[3], hs[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    blo[a] = center(K0[a], g.sp[a]);
+    bhi[a] = center(K0[a] + ext[a] - 1, g.sp[a]);
+    cc[a] = 0.5 * (blo[a] + bhi[a]);
+    hs[a] = 0.5 * (bhi[a] - blo[a]);
+  }
+  const long long nsbx = (g.n[0] + 7) / 8, nsby = (g.n[1] + 7) / 8;
+  auto sb_id = [&](long long x, long long y, long long z) {  // 8x8x4 sub-brick at voxel (x, y, z)
+    return (x >> 3) + nsbx * ((y >> 3) + nsby * ((z - g.z_begin) >> 2));
+  };
+  const double R = prm->gather_r;
+  const double cutoff = prm->cutoff;
+  float halfLf[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) halfLf[a] = (float)g.halfL[a];
+  const float invG = KIND == kVoronoi ? 1.f : (float)(1.0 / g.growth);
+  // absolute slack for f32 coordinates relative to the super-brick centre
+  const float e_d = (float)(1e-6 * (R + hs[0] + hs[1] + hs[2] + g.cw[0] + g.cw[1] + g.cw[2]));
+
+  // ---------------- G: gather ----------------
+  long long cl[3], ch[3];
+  bool full[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    cl[a] = (long long)floor((blo[a] - R) * g.inv_cw[a] - 1e-6);
+    ch[a] = (long long)floor((bhi[a] + R) * g.inv_cw[a] + 1e-6);
+    full[a] = false;
+    if (PER) {
+      if (ch[a] - cl[a] + 1 >= g.m[a]) {
+        cl[a] = 0;
+        ch[a] = g.m[a] - 1;
+        full[a] = true;
+      }
+    } else {
+      cl[a] = max(cl[a], 0ll);
+      ch[a] = min(ch[a], (long long)g.m[a] - 1);
+    }
+  }
+  const int nry = (int)(ch[1] - cl[1] + 1), nrz = (int)(ch[2] - cl[2] + 1);
+  const int nrows = nry * nrz;
+  const bool rows_ok = nry > 0 && nrz > 0 && nrows <= kRows2;
+  const double R2 = R * R;
+  if (rows_ok) {
+    for (int r = tid; r < nrows; r += kB2Threads) {
+      const long long cy = cl[1] + r % nry, cz = cl[2] + r / nry;
+      double dy = 0.0, dz = 0.0;
+      if (!full[1]) dy = fmax(0.0, fmax(cy * g.cw[1] - bhi[1], blo[1] - (cy + 1) * g.cw[1]));
+      if (!full[2]) dz = fmax(0.0, fmax(cz * g.cw[2] - bhi[2], blo[2] - (cz + 1) * g.cw[2]));
+      const double dyz = dy * dy + dz * dz;
+      int st0 = 0, n0 = 0, st1 = 0, n1 = 0;
+      if (dyz <= R2 * (1.0 + 1e-9)) {
+        const double exr = sqrt(fmax(R2 - dyz, 0.0)) * (1.0 + 1e-9) + 1e-12 * g.lmax;
+        const long long cx0 = (long long)floor((blo[0] - exr) * g.inv_cw[0] - 1e-6);
+        const long long cx1 = (long long)floor((bhi[0] + exr) * g.inv_cw[0] + 1e-6);
+        const long long wy = PER ? wrapi2(cy, g.m[1]) : cy, wz = PER ? wrapi2(cz, g.m[2]) : cz;
+        const long long base = (long long)g.m[0] * (wy + (long long)g.m[1] * wz);
+        const int mx = g.m[0];
+        long long a0 = 0, a1 = -1, c0 = 0, c1 = -1;
+        if (PER) {
+          if (cx1 - cx0 + 1 >= mx) {
+            a0 = 0;
+            a1 = mx - 1;
+          } else {
+            const long long w0 = wrapi2(cx0, mx), len = cx1 - cx0 + 1;
+            a0 = w0;
+            if (w0 + len <= mx) {
+              a1 = w0 + len - 1;
+            } else {
+              a1 = mx - 1;
+              c0 = 0;
+              c1 = len - (mx - w0) - 1;
+            }
+          }
+        } else {
+          a0 = max(cx0, 0ll);
+          a1 = min(cx1, (long long)mx - 1);
+        }
+        if (a1 >= a0) {
+          st0 = bins.cell_start[base + a0];
+          n0 = bins.cell_start[base + a1 + 1] - st0;
+        }
+        if (c1 >= c0) {
+          st1 = bins.cell_start[base + c0];
+          n1 = bins.cell_start[base + c1 + 1] - st1;
+        }
+      }
+      S.seg_start[2 * r] = st0;
+      S.seg_off[2 * r] = n0;
+      S.seg_start[2 * r + 1] = st1;
+      S.seg_off[2 * r + 1] = n1;
+    }
+  }
+  __syncthreads();
+  // exclusive scan of the segment counts (2 per thread)
+  const int nseg = rows_ok ? 2 * nrows : 0;
+  {
+    const int k0 = 2 * tid;
+    const int c0 = k0 < nseg ? S.seg_off[k0] : 0, c1 = k0 + 1 < nseg ? S.seg_off[k0 + 1] : 0;
+    int inc = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) S.warp_tot[wid] = inc;
+    __syncthreads();
+    int base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kB2Threads / 32; ++w) {
+      base += w < wid ? S.warp_tot[w] : 0;
+      tot += S.warp_tot[w];
+    }
+    const int ex = base + inc - c0 - c1;
+    if (k0 < nseg) S.seg_off[k0] = ex;
+    if (k0 + 1 < nseg) S.seg_off[k0 + 1] = ex + c0;
+    if (tid == 0) {
+      S.seg_off[nseg] = tot;
+      S.n_total = tot;
+    }
+  }
+  if (tid == 0) S.n_kept = 0;
+  if (tid < 2 * kSB + 16 * nbb) {  // exact voxel centres (geometry.hpp:58-60)
+    const int a = tid < kSB ? 0 : (tid < 2 * kSB ? 1 : 2), k = tid - a * kSB;
+    (a == 0 ? S.cx : a == 1 ? S.cy : S.cz)[k] = center(K0[a] + k, g.sp[a]);
+  }
+  __syncthreads();
+  const int Traw = S.n_total;
+  bool cta_ok = rows_ok && Traw > 0;
+  if (cta_ok) {
+    // Only sites that can reach some voxel of the super-brick within the
+    // cutoff are kept: a site whose prox exceeds the cutoff everywhere can
+    // neither be the winner of a resolved voxel nor make one unresolved.
+    const double tc = cutoff + 1e-9 * fabs(cutoff);
+    for (int f0 = 0; f0 < Traw; f0 += kB2Threads) {
+      const int f = f0 + tid;
+      bool keep = false;
+      int p = 0;
+      float uf[3] = {0.f, 0.f, 0.f};
+      unsigned fl = 0;
+      double tv = 0.0;
+      if (f < Traw) {
+        int lo = 0, hi = nseg - 1;  // largest k with off[k] <= f
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (S.seg_off[mid] <= f) lo = mid;
+          else hi = mid - 1;
+        }
+        p = S.seg_start[lo] + (f - S.seg_off[lo]);
+        const double sv[3] = {bins.x[p], bins.y[p], bins.z[p]};
+        double lb = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          double u = sv[a] - cc[a];
+          if (PER) {
+            u = u - floor(u * g.invL[a] + 0.5) * g.L[a];
+            if (fabs(u) + hs[a] >= g.halfL[a] * (1.0 - 1e-7) - 4.0 * e_d) fl |= 1u << a;
+          }
+          uf[a] = (float)u;
+          const double m = ((fl >> a) & 1u) ? 0.0 : fmax(fabs(u) - hs[a], 0.0);
+          lb += m * m;
+        }
+        double lbp = lb * (1.0 - 1e-9);
+        if (KIND != kVoronoi) {
+          tv = bins.t[p];
+          const double A = (KIND == kJohnsonMehl ? sqrt(lbp) : lbp) / g.growth * (1.0 - 1e-9);
+          lbp = A + tv - 1e-9 * fabs(tv);
+        }
+        keep = lbp <= tc;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      int base = 0;
+      if (lane == 0 && m) base = atomicAdd(&S.n_kept, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const int pos = base + __popc(m & ((1u << lane) - 1u));
+      if (keep && pos < kTcap) {
+        S.rel[pos] = make_float4(uf[0], uf[1], uf[2], (float)tv);
+        S.p[pos] = p;
+        S.idx[pos] = bins.idx[p];
+        S.flag[pos] = (unsigned char)fl;
+      }
+    }
+  }
+  __syncthreads();
+  const int T = S.n_kept;
+  if (T <= kTcap) {  // rank sort of the kept sites by site index (ties impossible)
+    for (int f = tid; f < T; f += kB2Threads) {
+      const int me = S.idx[f];
+      int rank = 0;
+      for (int k = 0; k < T; ++k) rank += S.idx[k] < me;
+      S.ord[rank] = (short)f;
+    }
+  }
+  __syncthreads();
+  if (VX_STATS_ON && tid == 0) {  // diagnostics: gathered sites per CTA
+    atomicAdd(&eval_slots[64], (unsigned long long)Traw);
+    atomicAdd(&eval_slots[65], (unsigned long long)T);
+    atomicAdd(&eval_slots[66], 1ull);
+    atomicMax(&eval_slots[71], (unsigned long long)T);
+  }
+  cta_ok = cta_ok && T > 0 && T <= kTcap;
+
+  // ---------------- W + S: per-warp column of nbb bricks ----------------
+  WarpSmem& ws = S.w[wid];
+  const int bxo = (wid & 1) * 8, byo = ((wid >> 1) & 1) * 8;
+
+  auto box_of = [&](int x0, int y0, int z0, int nx, int ny, int nz) {
+    FBox B;
+    const int o[3] = {x0, y0, z0}, n[3] = {nx, ny, nz};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double* ct = a == 0 ? S.cx : (a == 1 ? S.cy : S.cz);
+      const double l = ct[o[a]], h = ct[o[a] + n[a] - 1];
+      B.c[a] = (float)(0.5 * (l + h) - cc[a]);
+      B.h[a] = (float)(0.5 * (h - l)) * (1.f + kRel) + 2.f * e_d;
+    }
+    return B;
+  };
+
+  // merged tau / keep-mask passes over the gathered sites for all bricks of the column
+  const int ex0 = min(8, ext[0] - bxo), ex1 = min(8, ext[1] - byo);
+  float bzc[kMaxBB], bzh[kMaxBB], tau[kMaxBB];
+  bool bval[kMaxBB];
+  FBox Bxy;
+#pragma unroll
+  for (int b = 0; b < kMaxBB; ++b) {
+    const int bzo = (wid >> 2) * 8 + 16 * b;
+    const int ez = min(8, ext[2] - bzo);
+    bval[b] = b < nbb && ex0 > 0 && ex1 > 0 && ez > 0;
+    bzc[b] = 0.f;
+    bzh[b] = 0.f;
+    tau[b] = -1.f;
+    if (bval[b]) {
+      const FBox B = box_of(bxo, byo, bzo, ex0, ex1, ez);
+      Bxy = B;
+      bzc[b] = B.c[2];
+      bzh[b] = B.h[2];
+    }
+  }
+  bool col_any = false;
+#pragma unroll
+  for (int b = 0; b < kMaxBB; ++b) col_any |= bval[b];
+  if (!col_any) return;  // no barrier follows
+  if (cta_ok) {
+    float myub[kMaxBB];
+#pragma unroll
+    for (int b = 0; b < kMaxBB; ++b) myub[b] = __int_as_float(0x7f800000);
+    for (int f = lane; f < T; f += 32) {
+      const float4 s = S.rel[f];
+      const unsigned fl = S.flag[f];
+      float mx = fabsf(s.x - Bxy.c[0]) + Bxy.h[0];
+      float my = fabsf(s.y - Bxy.c[1]) + Bxy.h[1];
+      if (PER) {
+        mx = (fl & 1u) ? halfLf[0] : fminf(mx, halfLf[0]);
+        my = (fl & 2u) ? halfLf[1] : fminf(my, halfLf[1]);
+      }
+      const float bxy = __fmaf_rn(my, my, mx * mx);
+#pragma unroll
+      for (int b = 0; b < kMaxBB; ++b) {
+        if (b >= nbb) break;
+        float mz = fabsf(s.z - bzc[b]) + bzh[b];
+        if (PER) mz = (fl & 4u) ? halfLf[2] : fminf(mz, halfLf[2]);
+        const float ub = __fmaf_rn(mz, mz, bxy) * (1.f + kRel);
+        myub[b] = fminf(myub[b], KIND == kVoronoi ? ub
+                                                  : hi_add((KIND == kJohnsonMehl ? sqrtf(ub) : ub) * invG * (1.f + kRel),
+                                                           s.w + kRel * fabsf(s.w)));
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < kMaxBB; ++b) {
+      float t = myub[b];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t = fminf(t, __shfl_xor_sync(0xffffffffu, t, o));
+      tau[b] = t;
+    }
+    for (int f = lane; f < T; f += 32) {
+      const float4 s = S.rel[f];
+      const unsigned fl = S.flag[f];
+      float lx = fmaxf(fabsf(s.x - Bxy.c[0]) - Bxy.h[0], 0.f);
+      float ly = fmaxf(fabsf(s.y - Bxy.c[1]) - Bxy.h[1], 0.f);
+      if (PER) {
+        if (fl & 1u) lx = 0.f;
+        if (fl & 2u) ly = 0.f;
+      }
+      const float bxy = __fmaf_rn(ly, ly, lx * lx);
+      unsigned m = 0;
+#pragma unroll
+      for (int b = 0; b < kMaxBB; ++b) {
+        if (b >= nbb) break;
+        float lz = fmaxf(fabsf(s.z - bzc[b]) - bzh[b], 0.f);
+        if (PER && (fl & 4u)) lz = 0.f;
+        const float lb = __fmaf_rn(lz, lz, bxy) * (1.f - kRel);
+        const float lbp = KIND == kVoronoi ? lb
+                                           : lo_add((KIND == kJohnsonMehl ? sqrtf(lb) : lb) * invG * (1.f - kRel),
+                                                    s.w - kRel * fabsf(s.w));
+        if (bval[b] && lbp <= tau[b]) m |= 1u << b;
+      }
+      S.mk[wid][f] = (unsigned char)m;
+    }
+    __syncwarp();
+  }
+
+  for (int bb = 0; bb < nbb; ++bb) {  // no barrier below: warps run independently
+  const int bzo = (wid >> 2) * 8 + 16 * bb;
+  const int bext[3] = {ex0, ex1, min(8, ext[2] - bzo)};
+  if (bext[0] <= 0 || bext[1] <= 0 || bext[2] <= 0) continue;
+
+  int nW = 0;
+  bool brick_ok = cta_ok;
+  if (brick_ok) {
+    for (int f0 = 0; f0 < T; f0 += 32) {
+      const int f = f0 + lane < T ? S.ord[f0 + lane] : 0;
+      const bool keep = f0 + lane < T && ((S.mk[wid][f] >> bb) & 1u);
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      const int pos = nW + __popc(m & ((1u << lane) - 1u));
+      if (keep && pos < kWcap) ws.W[pos] = f;  // ballot order = ord order = site order
+      nW += __popc(m);
+    }
+    brick_ok = nW <= kWcap;
+    if (VX_STATS_ON && lane == 0) {
+      atomicAdd(&eval_slots[67], (unsigned long long)nW);
+      atomicAdd(&eval_slots[68], 1ull);
+      atomicMax(&eval_slots[72], (unsigned long long)nW);
+    }
+  }
+  __syncwarp();
+
+  for (int q = 0; q < 2; ++q) {
+    const int sy = byo, sz = bzo + q * 4;
+    const int sext[3] = {bext[0], bext[1], min(4, ext[2] - sz)};
+    if (sext[1] <= 0 || sext[2] <= 0) continue;
+    int n2 = 0;
+    if (brick_ok) {
+      const FBox Bs = box_of(bxo, sy, sz, sext[0], sext[1], sext[2]);
+      // one bound evaluation per brick-list site, kept in registers (slots
+      // lane and lane + 32; nW <= 64)
+      const bool va = lane < nW, vb = lane + 32 < nW;
+      const int fa = va ? ws.W[lane] : 0, fb = vb ? ws.W[lane + 32] : 0;
+      const unsigned fla = va ? S.flag[fa] : 0u, flb = vb ? S.flag[fb] : 0u;
+      SiteF sa, sb;
+      fbounds<KIND, PER>(S.rel[fa], fla, Bs, halfLf, invG, sa);
+      if (vb) fbounds<KIND, PER>(S.rel[fb], flb, Bs, halfLf, invG, sb);
+      // packed (upper bound, slot) arg-min -> reference s0 and tau = its ubp
+      auto okey = [](float v) -> unsigned {
+        const unsigned b = __float_as_uint(v);
+        return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+      };
+      unsigned km = min(va ? ((okey(sa.ubp) & ~63u) | (unsigned)lane) : 0xffffffffu,
+                        vb ? ((okey(sb.ubp) & ~63u) | (unsigned)(lane + 32)) : 0xffffffffu);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) km = min(km, __shfl_xor_sync(0xffffffffu, km, o));
+      const int r0 = (int)(km & 63u), rl = r0 & 31;
+      const bool rhi = r0 >= 32;
+      // broadcast the reference's bounds from its owner lane
+      SiteF z;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        z.v[a] = __shfl_sync(0xffffffffu, rhi ? sb.v[a] : sa.v[a], rl);
+        z.mn[a] = __shfl_sync(0xffffffffu, rhi ? sb.mn[a] : sa.mn[a], rl);
+        z.mx[a] = __shfl_sync(0xffffffffu, rhi ? sb.mx[a] : sa.mx[a], rl);
+      }
+      z.t = __shfl_sync(0xffffffffu, rhi ? sb.t : sa.t, rl);
+      z.lb = __shfl_sync(0xffffffffu, rhi ? sb.lb : sa.lb, rl);
+      z.ub = __shfl_sync(0xffffffffu, rhi ? sb.ub : sa.ub, rl);
+      const float tau = __shfl_sync(0xffffffffu, rhi ? sb.ubp : sa.ubp, rl);
+      const unsigned fl0 = __shfl_sync(0xffffffffu, rhi ? flb : fla, rl);
+      const bool ka = va && (lane == r0 || (sa.lbp <= tau &&
+                                            bisector_keep<KIND, PER>(sa, fla, z, fl0, Bs, halfLf, invG, e_d)));
+      const bool kb = vb && (lane + 32 == r0 || (sb.lbp <= tau &&
+                                                 bisector_keep<KIND, PER>(sb, flb, z, fl0, Bs, halfLf, invG, e_d)));
+      // survivors -> global list, in slot (= site index) order
+      const unsigned ma = __ballot_sync(0xffffffffu, ka), mb = __ballot_sync(0xffffffffu, kb);
+      n2 = __popc(ma) + __popc(mb);
+      int base = 0;
+      if (lane == 0 && n2 > 0 && n2 <= kFcap) base = atomicAdd(list_count, n2);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const bool ok = n2 <= kFcap && (long long)base + n2 <= list_cap;
+      if (ok) {
+        const unsigned lt = (1u << lane) - 1u;
+        if (ka) list[base + __popc(ma & lt)] = S.p[fa];
+        if (kb) list[base + __popc(ma) + __popc(mb & lt)] = S.p[fb];
+      }
+      if (VX_STATS_ON && lane == 0) {
+        atomicAdd(&eval_slots[69], (unsigned long long)n2);
+        atomicAdd(&eval_slots[70], 1ull);
+        atomicMax(&eval_slots[73], (unsigned long long)n2);
+      }
+      if (lane == 0) info[sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz)] = ok ? make_int2(base, n2) : make_int2(0, -1);
+    } else if (lane == 0) {
+      info[sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz)] = make_int2(0, -1);
+    }
+  }
+  if (lane == 0 && !(cta_ok && brick_ok)) atomicAdd(&ctr->overflow_bricks, 1ull);
+  }  // bb
+}
+
+constexpr int kEvalWarps = 8;
+
+// One warp per 8x8x4 sub-brick (the tail of v11's sub-brick loop: exact
+// tables, evaluation, stores, histogram, unresolved compaction).  The site
+// index load is issued before the tables and consumed at the store.
+template <int KIND, bool PER>
+__global__ void __launch_bounds__(kEvalWarps * 32, 4)
+    eval12_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, const int2* __restrict__ info,
+                  const int* __restrict__ list, int* __restrict__ labels, double* __restrict__ dist,
+                  unsigned long long* __restrict__ hist, long long* __restrict__ unres, long long unres_cap,
+                  DevCounters* ctr, unsigned long long* __restrict__ eval_slots, long long nsb) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  EvalSmem& ws = reinterpret_cast<EvalSmem*>(smem_raw)[wid];
+  const unsigned nsbx = (unsigned)((g.n[0] + 7) / 8), nsby = (unsigned)((g.n[1] + 7) / 8);
+  const double cutoff = prm->cutoff;
+  const long long slab_base = g.z_begin * g.n[0] * g.n[1];
+  const int qx = (lane & 1) * 4, vy = (lane >> 1) & 3, vz = lane >> 3;
+  const long long sb = (long long)blockIdx.x * kEvalWarps + wid;
+  if (sb >= nsb) return;
+  const int2 inf = info[sb];
+  const int pl = lane < inf.y ? list[inf.x + lane] : 0;
+  {
+    const unsigned usb = (unsigned)sb;
+    const unsigned sbx = usb % nsbx, sby = (usb / nsbx) % nsby, sbz = usb / (nsbx * nsby);
+    const long long x0 = (long long)sbx * 8, y0 = (long long)sby * 8, z0 = g.z_begin + (long long)sbz * 4;
+    const int sext[3] = {(int)min(8ll, g.n[0] - x0), (int)min(8ll, g.n[1] - y0), (int)min(4ll, g.z_end - z0)};
+    const int n2 = inf.y > 0 ? inf.y : 0;  // -1: overflow, every voxel goes to the shell search
+    int fidx = 0;
+    if (lane < n2) {
+      ws.P[lane] = pl;
+      ws.cnt[lane] = 0;
+      fidx = bins.idx[pl];
+      if (KIND != kVoronoi) ws.Ft[lane] = bins.t[pl];
+    }
+    __syncwarp();
+    // exact per-axis tables (the reference arithmetic): one lane per (site, axis)
+    for (int e = lane; e < 3 * n2; e += 32) {
+      const int a = e >= 2 * n2 ? 2 : (e >= n2 ? 1 : 0);
+      const int j = e - a * n2;
+      const int p = ws.P[j];
+      const double sv = a == 0 ? bins.x[p] : (a == 1 ? bins.y[p] : bins.z[p]);
+      const long long k0 = a == 0 ? x0 : (a == 1 ? y0 : z0);
+      const double spa = a == 0 ? g.sp[0] : (a == 1 ? g.sp[1] : g.sp[2]);
+      const double La = a == 0 ? g.L[0] : (a == 1 ? g.L[1] : g.L[2]);
+      const double iLa = a == 0 ? g.invL[0] : (a == 1 ? g.invL[1] : g.invL[2]);
+      const double lim = 0.49 * La;
+      double* trow = &ws.T[j][a * 8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        if (a == 2 && r >= 4) break;
+        const double u = __dsub_rn(sv, center(k0 + r, spa));  // geometry.hpp:58-60
+        // |u| < 0.49 L: floor(u*invL + 0.5) == 0, so the reference's wrap is u itself
+        const double w = (!PER || fabs(u) < lim) ? u : wrap_delta(u, La, iLa);
+        trow[r] = __dmul_rn(w, w);
+      }
+    }
+    __syncwarp();
+    // exact evaluation: lane -> 4 voxels along x in rows vy and vy + 4
+    double best[8];
+    int bj[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      best[k] = __longlong_as_double(0x7ff0000000000000ll);
+      bj[k] = -1;
+    }
+    const bool g1 = g.g_is_one;
+    for (int j = 0; j < n2; ++j) {
+      const double wz = ws.T[j][16 + vz];
+      const double a0 = __dadd_rn(wz, ws.T[j][8 + vy]);  // 0 + wz^2 == wz^2
+      const double a1 = __dadd_rn(wz, ws.T[j][12 + vy]);
+      const double2 w01 = *reinterpret_cast<const double2*>(&ws.T[j][qx]);
+      const double2 w23 = *reinterpret_cast<const double2*>(&ws.T[j][qx + 2]);
+      const double tj = KIND == kVoronoi ? 0.0 : ws.Ft[j];
+      const double d[8] = {__dadd_rn(a0, w01.x), __dadd_rn(a0, w01.y), __dadd_rn(a0, w23.x),
+                           __dadd_rn(a0, w23.y), __dadd_rn(a1, w01.x), __dadd_rn(a1, w01.y),
+                           __dadd_rn(a1, w23.x), __dadd_rn(a1, w23.y)};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double pr = prox_from_dsq<KIND>(d[k], g.growth, g1, tj);
+        if (pr < best[k]) {
+          best[k] = pr;
+          bj[k] = j;
+        }
+      }
+    }
+    // resolve + store + compaction of unresolved voxels
+    if (lane < n2) ws.Fidx[lane] = fidx;  // its load was issued before the tables
+    __syncwarp();
+    const long long kz = z0 + vz;
+    const long long lin0 = x0 + qx + g.n[0] * (y0 + vy + g.n[1] * kz);
+    const long long rstep = 4 * g.n[0];  // row vy -> vy + 4
+    int lab[8];
+    unsigned umask = 0;  // bit k: voxel k valid but unresolved
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      lab[k] = -1;
+      const bool valid = (k < 4 ? vy : vy + 4) < sext[1] && vz < sext[2] && qx + (k & 3) < sext[0];
+      if (valid) {
+        if (best[k] <= cutoff) {  // best = +inf when there is no candidate
+          lab[k] = ws.Fidx[bj[k]];
+          if (hist) atomicAdd(&ws.cnt[bj[k]], 1);
+        } else {
+          umask |= 1u << k;
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const bool rv = (vy + 4 * h) < sext[1] && vz < sext[2];
+      if (!rv) continue;
+      int* out = labels + (lin0 + h * rstep - slab_base);
+      if (qx + 4 <= sext[0] && g.vec_store) {
+        *reinterpret_cast<int4*>(out) = make_int4(lab[4 * h], lab[4 * h + 1], lab[4 * h + 2], lab[4 * h + 3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (qx + k < sext[0]) out[k] = lab[4 * h + k];
+      }
+      if (dist) {
+        double* dout = dist + (lin0 + h * rstep - slab_base);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (qx + k < sext[0] && lab[4 * h + k] >= 0)
+            dout[k] = KIND == kVoronoi ? __dsqrt_rn(best[4 * h + k]) : best[4 * h + k];
+      }
+    }
+    if (__any_sync(0xffffffffu, umask != 0)) {  // K3: compaction of unresolved voxels
+      const int nun = __popc(umask);
+      int inc = nun;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const int wtot = __shfl_sync(0xffffffffu, inc, 31);
+      unsigned long long base = 0;
+      if (lane == 31) base = atomicAdd(&ctr->n_unres, (unsigned long long)wtot);
+      base = __shfl_sync(0xffffffffu, base, 31);
+      const long long off = (long long)base + inc - nun;
+      unsigned mm = umask;
+      for (int i = 0; i < nun; ++i) {
+        const int k = __ffs(mm) - 1;
+        mm &= mm - 1;
+        if (off + i < unres_cap) unres[off + i] = lin0 + (k < 4 ? 0 : rstep) + (k & 3);
+      }
+    }
+    if (lane == 0 && n2)
+      atomicAdd(&eval_slots[sb & 63], (unsigned long long)n2 * (sext[0] * sext[1] * sext[2]));
+    if (hist && n2 > 0) {
+      __syncwarp();
+      if (lane < n2 && ws.cnt[lane]) atomicAdd(&hist[ws.Fidx[lane]], (unsigned long long)ws.cnt[lane]);
+    }
+  }
+}
+
+}  // namespace v12
+
+__global__ void ball12_publish_kernel(const unsigned long long* slots, DevCounters* ctr) {
+  unsigned long long s = 0;
+  for (int i = threadIdx.x; i < 64; i += 32) s += slots[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (threadIdx.x == 0) ctr->ball_evals += s;
+}
+
+// Bricks per warp column: the tallest column (fewest gathers) whose expected
+// gathered list stays well inside kTcap.  Sites per super-brick ~ density x
+// (super-brick + a gather margin of ~1.6 site spacings on every side).
+static int choose_nbb12(const Geo& g) {
+  double L3 = 1.0;
+  for (int a = 0; a < 3; ++a) L3 *= g.L[a];
+  const double lambda = (double)g.n_sites / L3;
+  const double spacing = pow(g.vol_true / (double)(g.n_sites > 0 ? g.n_sites : 1), 1.0 / g.dim);
+  const double R = 1.6 * spacing;
+  for (int nbb = v12::kMaxBB; nbb > 1; nbb >>= 1) {
+    double vol = 1.0;
+    for (int a = 0; a < 3; ++a) {
+      const long long ev = a < 2 ? v12::kSB : 16 * nbb;
+      const double e = (double)(g.n[a] < ev ? g.n[a] : ev) * g.sp[a] + (g.n[a] > 1 ? 2.0 * R : 0.0);
+      vol *= e < g.L[a] ? e : g.L[a];
+    }
+    if (0.7 * lambda * vol <= 0.5 * v12::kTcap) return nbb;
+  }
+  return 1;
+}
+
+long long ball12_subbricks(const Geo& g) {
+  return ((g.n[0] + 7) / 8) * ((g.n[1] + 7) / 8) * ((g.z_end - g.z_begin + 3) / 4);
+}
+
+template <int KIND, bool PER>
+static void launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* labels, double* dist,
+                     unsigned long long* hist, long long* unres, long long cap, DevCounters* ctr,
+                     unsigned long long* slots, int2* info, int* list, long long list_cap, int* list_count,
+                     int nbb, cudaStream_t st) {
+  static bool attr = false;
+  const size_t sh_c = sizeof(v12::Smem2);
+  const size_t sh_e = sizeof(v12::EvalSmem) * v12::kEvalWarps;
+  if (!attr) {
+    cudaFuncSetAttribute(v12::cull12_kernel<KIND, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_c);
+    cudaFuncSetAttribute(v12::eval12_kernel<KIND, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_e);
+    attr = true;
+  }
+  const dim3 grid((unsigned)((g.n[0] + v12::kSB - 1) / v12::kSB), (unsigned)((g.n[1] + v12::kSB - 1) / v12::kSB),
+                  (unsigned)((g.z_end - g.z_begin + 16 * nbb - 1) / (16 * nbb)));
+  v12::cull12_kernel<KIND, PER><<<grid, v12::kB2Threads, sh_c, st>>>(g, bins, prm, info, list, list_cap, list_count,
+                                                                     ctr, slots, nbb);
+  const long long nsb = ball12_subbricks(g);
+  const long long want = (nsb + v12::kEvalWarps - 1) / v12::kEvalWarps;
+  const unsigned eb = (unsigned)want;
+  v12::eval12_kernel<KIND, PER><<<eb, v12::kEvalWarps * 32, sh_e, st>>>(g, bins, prm, info, list, labels, dist,
+                                                                        hist, unres, cap, ctr, slots, nsb);
+}
+
+int launch_ball12(const Geo& g, const Bins& bins, const DevParams* prm, int* labels, double* dist,
+                  unsigned long long* hist, long long* unres, long long unres_cap, DevCounters* ctr,
+                  unsigned long long* slots, int2* info, int* list, long long list_cap, int* list_count,
+                  cudaStream_t st) {
+  if (g.z_end <= g.z_begin) return 0;
+  cudaMemsetAsync(slots, 0, 128 * sizeof(unsigned long long), st);
+  cudaMemsetAsync(list_count, 0, sizeof(int), st);
+  static const int nbb_env = std::getenv("VX_NBB") ? std::atoi(std::getenv("VX_NBB")) : 0;
+  const int nbb = nbb_env == 1 || nbb_env == 2 || nbb_env == 4 ? nbb_env : choose_nbb12(g);
+#define VX_L12(K, P) launch12<K, P>(g, bins, prm, labels, dist, hist, unres, unres_cap, ctr, slots, info, list, \
+                                    list_cap, list_count, nbb, st)
+  switch (g.kind * 2 + (g.periodic ? 1 : 0)) {
+    case 0: VX_L12(kVoronoi, false); break;
+    case 1: VX_L12(kVoronoi, true); break;
+    case 2: VX_L12(kJohnsonMehl, false); break;
+    case 3: VX_L12(kJohnsonMehl, true); break;
+    case 4: VX_L12(kLaguerre, false); break;
+    default: VX_L12(kLaguerre, true); break;
+  }
+#undef VX_L12
+  ball12_publish_kernel<<<1, 32, 0, st>>>(slots, ctr);
+  return 3;
+}
+
+}  // namespace vxb

@@ -59,7 +59,7 @@ struct vx_context {
   std::mutex mu;
   Buf pos_raw, t_raw, w_raw, p3, t, dropped, keys_a, keys_b, vals_a, vals_b, bx, by, bz, bt, bidx,
       cell_start, cub, labels, dist, hist, unres, params, counters, scratch, vsample, vlab, vdist,
-      vbad, slots, f4;
+      vbad, slots, f4, sb_info, sb_list, sb_count;
   DevParams* h_prm = nullptr;
   DevCounters* h_ctr = nullptr;
   cudaEvent_t ev[8] = {};  // stage markers (options.profile_stages)
@@ -70,10 +70,11 @@ struct vx_context {
   void* pin[2] = {};                   // pinned double buffer of the file writer
   size_t pin_bytes = 0;
 
-  Buf* all[30] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
+  Buf* all[33] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
                   &vals_a,  &vals_b,  &bx,    &by,    &bz,     &bt,      &bidx,     &cell_start,
                   &cub,     &labels,  &dist,  &hist,  &unres,  &params,  &counters, &scratch,
-                  &vsample, &vlab,    &vdist, &vbad,  &slots,  &f4};
+                  &vsample, &vlab,    &vdist, &vbad,  &slots,  &f4,      &sb_info,  &sb_list,
+                  &sb_count};
 };
 
 namespace {
@@ -625,12 +626,19 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
                                 ball_scale, scratch, st);
       dbg(st, "params");
       tm.mark(3);
-      static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 11;
+      static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 12;
       static const int bzw = std::getenv("VX_BZW") ? std::atoi(std::getenv("VX_BZW")) : 4;
       static const int sy = std::getenv("VX_SY") ? std::atoi(std::getenv("VX_SY")) : 4;
       auto ball_and_shell = [&](const Geo& gg, int32_t* lb, double* ds) {
         unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
-        if (ball_ver == 11) launches += launch_ball11(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
+        if (ball_ver == 12) {
+          const long long nsb = ball12_subbricks(gg);
+          int2* info = ensure<int2>(ctx->sb_info, (size_t)nsb);
+          const long long lcap = std::min<long long>(nsb * 16 + (1 << 20), (1ll << 31) - 1);
+          int* list = ensure<int>(ctx->sb_list, (size_t)lcap);
+          int* lcount = ensure<int>(ctx->sb_count, 1);
+          launches += launch_ball12(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, info, list, lcap, lcount, st);
+        } else if (ball_ver == 11) launches += launch_ball11(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
         else if (ball_ver == 10) launches += launch_ball10(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
         else if (ball_ver == 9) launches += launch_ball9(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
         else if (ball_ver == 8) launches += launch_ball8(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
