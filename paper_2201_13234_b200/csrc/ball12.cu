@@ -69,6 +69,7 @@ constexpr int kB2Threads = 256;   // 8 warps, one 8^3 brick each
 constexpr int kTcap = 512;        // sites kept per super-brick (else the CTA falls back)
 constexpr int kWcap = 64;         // brick-level survivors per warp (2 slots per lane)
 constexpr int kFcap = 32;         // sub-brick survivors per warp (exact stage)
+constexpr int kSlot = 16;         // fixed list slots per sub-brick (longer lists: overflow list)
 constexpr int kRows2 = 256;       // cell rows per super-brick
 constexpr float kRel = 1e-5f;
 
@@ -214,7 +215,7 @@ __device__ __forceinline__ long long wrapi2(long long c, long long m) {
 template <int KIND, bool PER>
 __global__ void __launch_bounds__(kB2Threads, 4)
     cull12_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, int2* __restrict__ info,
-                  int* __restrict__ list, long long list_cap, int* __restrict__ list_count,
+                  int* __restrict__ slots16, int* __restrict__ list, long long list_cap, int* __restrict__ list_count,
                   DevCounters* ctr, unsigned long long* __restrict__ eval_slots, int nbb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem2& S = *reinterpret_cast<Smem2*>(smem_raw);
@@ -597,24 +598,27 @@ __global__ void __launch_bounds__(kB2Threads, 4)
                                             bisector_keep<KIND, PER>(sa, fla, z, fl0, Bs, halfLf, invG, e_d)));
       const bool kb = vb && (lane + 32 == r0 || (sb.lbp <= tau &&
                                                  bisector_keep<KIND, PER>(sb, flb, z, fl0, Bs, halfLf, invG, e_d)));
-      // survivors -> global list, in slot (= site index) order
+      // survivors -> the sub-brick's kSlot fixed slots (or the overflow
+      // list when longer), in slot (= site index) order
+      const long long sbi = sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz);
       const unsigned ma = __ballot_sync(0xffffffffu, ka), mb = __ballot_sync(0xffffffffu, kb);
       n2 = __popc(ma) + __popc(mb);
       int base = 0;
-      if (lane == 0 && n2 > 0 && n2 <= kFcap) base = atomicAdd(list_count, n2);
+      if (lane == 0 && n2 > kSlot && n2 <= kFcap) base = atomicAdd(list_count, n2);
       base = __shfl_sync(0xffffffffu, base, 0);
-      const bool ok = n2 <= kFcap && (long long)base + n2 <= list_cap;
+      const bool ok = n2 <= kFcap && (n2 <= kSlot || (long long)base + n2 <= list_cap);
       if (ok) {
         const unsigned lt = (1u << lane) - 1u;
-        if (ka) list[base + __popc(ma & lt)] = S.p[fa];
-        if (kb) list[base + __popc(ma) + __popc(mb & lt)] = S.p[fb];
+        int* dst = n2 <= kSlot ? slots16 + sbi * kSlot : list + base;
+        if (ka) dst[__popc(ma & lt)] = S.p[fa];
+        if (kb) dst[__popc(ma) + __popc(mb & lt)] = S.p[fb];
       }
       if (VX_STATS_ON && lane == 0) {
         atomicAdd(&eval_slots[69], (unsigned long long)n2);
         atomicAdd(&eval_slots[70], 1ull);
         atomicMax(&eval_slots[73], (unsigned long long)n2);
       }
-      if (lane == 0) info[sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz)] = ok ? make_int2(base, n2) : make_int2(0, -1);
+      if (lane == 0) info[sbi] = ok ? make_int2(base, n2) : make_int2(0, -1);
     } else if (lane == 0) {
       info[sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz)] = make_int2(0, -1);
     }
@@ -623,7 +627,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
   }  // bb
 }
 
-constexpr int kEvalWarps = 8;
+constexpr int kEvalWarps = 8;  // sub-bricks along y per CTA
 
 // One warp per 8x8x4 sub-brick (the tail of v11's sub-brick loop: exact
 // tables, evaluation, stores, histogram, unresolved compaction).  The site
@@ -631,7 +635,8 @@ constexpr int kEvalWarps = 8;
 template <int KIND, bool PER>
 __global__ void __launch_bounds__(kEvalWarps * 32, 4)
     eval12_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, const int2* __restrict__ info,
-                  const int* __restrict__ list, int* __restrict__ labels, double* __restrict__ dist,
+                  const int* __restrict__ slots16, const int* __restrict__ list, int* __restrict__ labels,
+                  double* __restrict__ dist,
                   unsigned long long* __restrict__ hist, long long* __restrict__ unres, long long unres_cap,
                   DevCounters* ctr, unsigned long long* __restrict__ eval_slots, long long nsb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -641,13 +646,14 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 4)
   const double cutoff = prm->cutoff;
   const long long slab_base = g.z_begin * g.n[0] * g.n[1];
   const int qx = (lane & 1) * 4, vy = (lane >> 1) & 3, vz = lane >> 3;
-  const long long sb = (long long)blockIdx.x * kEvalWarps + wid;
-  if (sb >= nsb) return;
+  // grid (nsbx, ceil(nsby / 8), nsbz): no index division
+  const unsigned sbx = blockIdx.x, sby = blockIdx.y * kEvalWarps + wid, sbz = blockIdx.z;
+  if (sby >= nsby) return;
+  const long long sb = (long long)sbx + (long long)nsbx * ((long long)sby + (long long)nsby * sbz);
   const int2 inf = info[sb];
-  const int pl = lane < inf.y ? list[inf.x + lane] : 0;
+  const int ps = lane < kSlot ? slots16[sb * kSlot + lane] : 0;  // issued with info, not after it
+  const int pl = inf.y > kSlot ? (lane < inf.y ? list[inf.x + lane] : 0) : ps;
   {
-    const unsigned usb = (unsigned)sb;
-    const unsigned sbx = usb % nsbx, sby = (usb / nsbx) % nsby, sbz = usb / (nsbx * nsby);
     const long long x0 = (long long)sbx * 8, y0 = (long long)sby * 8, z0 = g.z_begin + (long long)sbz * 4;
     const int sext[3] = {(int)min(8ll, g.n[0] - x0), (int)min(8ll, g.n[1] - y0), (int)min(4ll, g.z_end - z0)};
     const int n2 = inf.y > 0 ? inf.y : 0;  // -1: overflow, every voxel goes to the shell search
@@ -712,6 +718,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 4)
     // resolve + store + compaction of unresolved voxels
     if (lane < n2) ws.Fidx[lane] = fidx;  // its load was issued before the tables
     __syncwarp();
+
     const long long kz = z0 + vz;
     const long long lin0 = x0 + qx + g.n[0] * (y0 + vy + g.n[1] * kz);
     const long long rstep = 4 * g.n[0];  // row vy -> vy + 4
@@ -817,8 +824,8 @@ long long ball12_subbricks(const Geo& g) {
 template <int KIND, bool PER>
 static void launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* labels, double* dist,
                      unsigned long long* hist, long long* unres, long long cap, DevCounters* ctr,
-                     unsigned long long* slots, int2* info, int* list, long long list_cap, int* list_count,
-                     int nbb, cudaStream_t st) {
+                     unsigned long long* slots, int2* info, int* slots16, int* list, long long list_cap,
+                     int* list_count, int nbb, cudaStream_t st) {
   static bool attr = false;
   const size_t sh_c = sizeof(v12::Smem2);
   const size_t sh_e = sizeof(v12::EvalSmem) * v12::kEvalWarps;
@@ -829,26 +836,26 @@ static void launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* 
   }
   const dim3 grid((unsigned)((g.n[0] + v12::kSB - 1) / v12::kSB), (unsigned)((g.n[1] + v12::kSB - 1) / v12::kSB),
                   (unsigned)((g.z_end - g.z_begin + 16 * nbb - 1) / (16 * nbb)));
-  v12::cull12_kernel<KIND, PER><<<grid, v12::kB2Threads, sh_c, st>>>(g, bins, prm, info, list, list_cap, list_count,
-                                                                     ctr, slots, nbb);
+  v12::cull12_kernel<KIND, PER><<<grid, v12::kB2Threads, sh_c, st>>>(g, bins, prm, info, slots16, list, list_cap,
+                                                                     list_count, ctr, slots, nbb);
   const long long nsb = ball12_subbricks(g);
-  const long long want = (nsb + v12::kEvalWarps - 1) / v12::kEvalWarps;
-  const unsigned eb = (unsigned)want;
-  v12::eval12_kernel<KIND, PER><<<eb, v12::kEvalWarps * 32, sh_e, st>>>(g, bins, prm, info, list, labels, dist,
-                                                                        hist, unres, cap, ctr, slots, nsb);
+  const dim3 eg((unsigned)((g.n[0] + 7) / 8), (unsigned)(((g.n[1] + 7) / 8 + v12::kEvalWarps - 1) / v12::kEvalWarps),
+                (unsigned)((g.z_end - g.z_begin + 3) / 4));
+  v12::eval12_kernel<KIND, PER><<<eg, v12::kEvalWarps * 32, sh_e, st>>>(g, bins, prm, info, slots16, list, labels,
+                                                                        dist, hist, unres, cap, ctr, slots, nsb);
 }
 
 int launch_ball12(const Geo& g, const Bins& bins, const DevParams* prm, int* labels, double* dist,
                   unsigned long long* hist, long long* unres, long long unres_cap, DevCounters* ctr,
-                  unsigned long long* slots, int2* info, int* list, long long list_cap, int* list_count,
-                  cudaStream_t st) {
+                  unsigned long long* slots, int2* info, int* slots16, int* list, long long list_cap,
+                  int* list_count, cudaStream_t st) {
   if (g.z_end <= g.z_begin) return 0;
   cudaMemsetAsync(slots, 0, 128 * sizeof(unsigned long long), st);
   cudaMemsetAsync(list_count, 0, sizeof(int), st);
   static const int nbb_env = std::getenv("VX_NBB") ? std::atoi(std::getenv("VX_NBB")) : 0;
   const int nbb = nbb_env == 1 || nbb_env == 2 || nbb_env == 4 ? nbb_env : choose_nbb12(g);
-#define VX_L12(K, P) launch12<K, P>(g, bins, prm, labels, dist, hist, unres, unres_cap, ctr, slots, info, list, \
-                                    list_cap, list_count, nbb, st)
+#define VX_L12(K, P) launch12<K, P>(g, bins, prm, labels, dist, hist, unres, unres_cap, ctr, slots, info, slots16, \
+                                    list, list_cap, list_count, nbb, st)
   switch (g.kind * 2 + (g.periodic ? 1 : 0)) {
     case 0: VX_L12(kVoronoi, false); break;
     case 1: VX_L12(kVoronoi, true); break;
