@@ -25,10 +25,16 @@ METRICS = {
 
 
 def raw(rep):
+    """Per-kernel metric dicts of every launch in the report."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
+    return [(vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?", one(hdr, units, vals))
+            for vals in rows[2:] if len(vals) == len(hdr)]
+
+
+def one(hdr, units, vals):
     res = {}
     for k, m in METRICS.items():
         if m in hdr:
@@ -45,13 +51,8 @@ def raw(rep):
     return res
 
 
-def main():
-    rep, cfg, label = sys.argv[1], sys.argv[2], sys.argv[3]
-    r = raw(rep)
-    entry = {
-        "kernel": label,
-        "report": os.path.basename(rep),
-        "ball_dram_bytes_per_launch": r.get("dram_read_bytes", 0.0) + r.get("dram_write_bytes", 0.0),
+def summarise(r):
+    return {
         "dram_read_bytes": r.get("dram_read_bytes"),
         "dram_write_bytes": r.get("dram_write_bytes"),
         "duration_ms_under_ncu": r.get("duration_ns", 0.0) / 1e6,
@@ -60,6 +61,23 @@ def main():
         "issued_ipc": r.get("issued_ipc"),
         "fp64_pipe_pct": r.get("fp64_pipe_pct"),
         "warp_instructions": r.get("warp_instructions"),
+    }
+
+
+def main():
+    rep, cfg, label = sys.argv[1], sys.argv[2], sys.argv[3]
+    launches = raw(rep)
+    total = lambda k: sum(r.get(k, 0.0) or 0.0 for _, r in launches)  # noqa: E731
+    entry = {
+        "kernel": label,
+        "report": os.path.basename(rep),
+        # one ball phase = every kernel launch captured in the report
+        "ball_dram_bytes_per_launch": total("dram_read_bytes") + total("dram_write_bytes"),
+        "dram_read_bytes": total("dram_read_bytes"),
+        "dram_write_bytes": total("dram_write_bytes"),
+        "duration_ms_under_ncu": total("duration_ns") / 1e6,
+        "warp_instructions": total("warp_instructions"),
+        "kernels": {name.split("<")[0].split("(")[0].split("::")[-1].split()[-1]: summarise(r) for name, r in launches},
     }
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     d = {}
