@@ -627,13 +627,13 @@ __global__ void __launch_bounds__(kB2Threads, 4)
   }  // bb
 }
 
-constexpr int kEvalWarps = 8;  // sub-bricks along y per CTA
+constexpr int kEvalWarps = 2;  // sub-bricks along y per CTA
 
 // One warp per 8x8x4 sub-brick (the tail of v11's sub-brick loop: exact
 // tables, evaluation, stores, histogram, unresolved compaction).  The site
 // index load is issued before the tables and consumed at the store.
 template <int KIND, bool PER>
-__global__ void __launch_bounds__(kEvalWarps * 32, 4)
+__global__ void __launch_bounds__(kEvalWarps * 32, 16)
     eval12_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, const int2* __restrict__ info,
                   const int* __restrict__ slots16, const int* __restrict__ list, int* __restrict__ labels,
                   double* __restrict__ dist,
