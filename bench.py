@@ -364,7 +364,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-planes", type=int, default=32)
+    ap.add_argument("--cpu-planes", type=int, default=320)  # ~10 s of reference CPU work at cfg5
     ap.add_argument("--ref-planes", type=int, default=32)
     # functional dry run of the N > 1 path on a one-GPU box (not a measurement):
     # gloo collectives, every rank on cuda:0
