@@ -627,8 +627,6 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       dbg(st, "params");
       tm.mark(3);
       static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 12;
-      static const int bzw = std::getenv("VX_BZW") ? std::atoi(std::getenv("VX_BZW")) : 4;
-      static const int sy = std::getenv("VX_SY") ? std::atoi(std::getenv("VX_SY")) : 4;
       auto ball_and_shell = [&](const Geo& gg, int32_t* lb, double* ds) {
         unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
         if (ball_ver == 12) {
@@ -640,17 +638,11 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
           int* lcount = ensure<int>(ctx->sb_count, 1);
           launches += launch_ball12(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, info, slots16, list, lcap,
                                     lcount, st);
-        } else if (ball_ver == 11) launches += launch_ball11(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
-        else if (ball_ver == 10) launches += launch_ball10(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
-        else if (ball_ver == 9) launches += launch_ball9(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
-        else if (ball_ver == 8) launches += launch_ball8(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
-        else if (ball_ver == 7) launches += launch_ball7(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
-        else if (ball_ver == 6) launches += launch_ball6(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
-        else if (ball_ver == 5) launches += launch_ball5(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, sy, st);
-        else if (ball_ver == 1) launches += launch_ball(gg, bins, prm, lb, ds, hist, unres, cap, ctr, st);
-        else if (ball_ver == 4) launches += launch_ball4(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
-        else if (ball_ver == 3) launches += launch_ball3(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, bzw, st);
-        else launches += launch_ball2(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
+        } else if (ball_ver == 11) {
+          launches += launch_ball11(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
+        } else {
+          launches += launch_ball(gg, bins, prm, lb, ds, hist, unres, cap, ctr, st);
+        }
         dbg(st, "ball");
         tm.mark(4);
         launches += launch_shell(gg, bins, prm, lb, ds, hist, unres, cap, ctr, st);

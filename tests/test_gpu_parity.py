@@ -323,7 +323,7 @@ def test_baseline_config_fingerprints(oracle_mod, k):
         assert np.array_equal(r.labels.labels, ref)
 
 
-@pytest.mark.parametrize("ver", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12])
+@pytest.mark.parametrize("ver", [1, 11, 12])
 def test_every_ball_kernel_variant(ver):
     """Each ball-kernel generation stays bit-exact (selected with VX_BALL)."""
     code = r"""
