@@ -36,6 +36,7 @@
 // f32 bounds: every bound is widened by kRel (1e-5) relative to the magnitude
 // of its terms plus an absolute coordinate slack e_d; float rounding is ~1e-7
 // relative, so a site is only culled if it loses by >> f64 rounding.
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 
@@ -769,12 +770,17 @@ template <int KIND, bool PER>
 static void launch11(const Geo& g, const Bins& bins, const DevParams* prm, int* labels,
                     double* dist, unsigned long long* hist, long long* unres, long long cap,
                     DevCounters* ctr, unsigned long long* slots, int nbb, cudaStream_t st) {
-  static bool attr = false;
+  // the dynamic-smem opt-in is per device: remember it per device ordinal
+  static std::atomic<unsigned long long> attr_done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  const bool attr = (attr_done.load() & bit) != 0;
   const size_t sh = sizeof(v11::Smem2);
   if (!attr) {
     cudaFuncSetAttribute(v11::ball11_kernel<KIND, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sh);
-    attr = true;
+    attr_done.fetch_or(bit);
   }
   const dim3 grid((unsigned)((g.n[0] + v11::kSB - 1) / v11::kSB), (unsigned)((g.n[1] + v11::kSB - 1) / v11::kSB),
                   (unsigned)((g.z_end - g.z_begin + 16 * nbb - 1) / (16 * nbb)));

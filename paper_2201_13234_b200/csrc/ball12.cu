@@ -51,6 +51,7 @@
 // of its terms plus an absolute coordinate slack e_d; float rounding is ~1e-7
 // relative, so a site is only culled if it loses by >> f64 rounding.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 
@@ -826,13 +827,18 @@ static void launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* 
                      unsigned long long* hist, long long* unres, long long cap, DevCounters* ctr,
                      unsigned long long* slots, int2* info, int* slots16, int* list, long long list_cap,
                      int* list_count, int nbb, cudaStream_t st) {
-  static bool attr = false;
+  // the dynamic-smem opt-in is per device: remember it per device ordinal
+  static std::atomic<unsigned long long> attr_done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  const bool attr = (attr_done.load() & bit) != 0;
   const size_t sh_c = sizeof(v12::Smem2);
   const size_t sh_e = sizeof(v12::EvalSmem) * v12::kEvalWarps;
   if (!attr) {
     cudaFuncSetAttribute(v12::cull12_kernel<KIND, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_c);
     cudaFuncSetAttribute(v12::eval12_kernel<KIND, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_e);
-    attr = true;
+    attr_done.fetch_or(bit);
   }
   const dim3 grid((unsigned)((g.n[0] + v12::kSB - 1) / v12::kSB), (unsigned)((g.n[1] + v12::kSB - 1) / v12::kSB),
                   (unsigned)((g.z_end - g.z_begin + 16 * nbb - 1) / (16 * nbb)));
