@@ -755,6 +755,10 @@ static int choose_nbb(const Geo& g) {
   const double spacing = pow(g.vol_true / (double)(g.n_sites > 0 ? g.n_sites : 1), 1.0 / g.dim);
   const double R = 1.6 * spacing;
   for (int nbb = v11::kMaxBB; nbb > 1; nbb >>= 1) {
+    // periodic: a gathered site is within hs + R of the super-brick centre, and
+    // the culling bounds need |u| + hs < L/2 (else the axis is treated as
+    // ambiguous and nothing is culled along it)
+    if (g.periodic && (double)(16 * nbb) * g.sp[2] + R >= 0.45 * g.L[2]) continue;
     double vol = 1.0;
     for (int a = 0; a < 3; ++a) {
       const long long ev = a < 2 ? v11::kSB : 16 * nbb;
