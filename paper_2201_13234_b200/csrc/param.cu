@@ -13,6 +13,7 @@
 namespace vxb {
 
 constexpr int kScan = 256;
+constexpr long long kCostSample = 8192;
 
 __global__ void init_kernel(DevParams* prm, DevCounters* ctr) {
   prm->tmin_key = ~0ull;
@@ -79,11 +80,19 @@ __global__ void cost_scan_kernel(CostArgs a, const double* __restrict__ bt,
   scan_range(a, prm, costs, pass, &lo, &hi);
   const double t0 = lo + (hi - lo) * blockIdx.x / (kScan - 1);
   const long long n = (long long)ctr->n_alive;
+  // t0 only sizes the ball phase (labels never depend on it): an evenly
+  // strided sample of <= kCostSample sites estimates the sums (binned order is
+  // spatial, independent of the birth times), scaled back to n
+  const long long m = n < kCostSample ? n : kCostSample;
   double sum = 0.0, lg = 0.0;
-  for (long long s = threadIdx.x; s < n; s += blockDim.x) {
-    const double f = site_frac(a, t0, bt[s]);
+  for (long long i = threadIdx.x; i < m; i += blockDim.x) {
+    const double f = site_frac(a, t0, bt[i * n / m]);
     sum += f;
     lg += log1p(-f);
+  }
+  if (m < n) {
+    sum *= (double)n / (double)m;
+    lg *= (double)n / (double)m;
   }
   for (int o = 16; o > 0; o >>= 1) {
     sum += __shfl_xor_sync(0xffffffffu, sum, o);
