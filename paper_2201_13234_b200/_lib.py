@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvoxellate_b200_debug.so" if os.environ.get("VX_LIB") == "debug" else "libvoxellate_b200.so")
+# VX_LIB=debug: the bounds-checked build; VX_LIB_PATH: an explicit library (A/B timing of builds)
+LIB_PATH = os.environ.get("VX_LIB_PATH") or os.path.join(
+    HERE, "libvoxellate_b200_debug.so" if os.environ.get("VX_LIB") == "debug" else "libvoxellate_b200.so")
 
 VX_OK, VX_EINVAL, VX_ECUDA, VX_ENOMEM, VX_EUNSUPPORTED, VX_EIO = 0, 1, 2, 3, 4, 5
 VX_MAX_DIM = 16

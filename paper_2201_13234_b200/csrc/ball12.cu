@@ -69,7 +69,8 @@ constexpr int kSZ = 16 * kMaxBB;
 constexpr int kB2Threads = 256;   // 8 warps, one 8^3 brick each
 constexpr int kTcap = 512;        // sites kept per super-brick (else the CTA falls back)
 constexpr int kWcap = 64;         // brick-level survivors per warp (2 slots per lane)
-constexpr int kFcap = 32;         // sub-brick survivors per warp (exact stage)
+constexpr int kFcap = 32;         // sub-brick survivors the eval kernel evaluates
+constexpr int kLcap = 64;         // sub-brick list capacity (<= the brick list's kWcap)
 constexpr int kSlot = 16;         // fixed list slots per sub-brick (longer lists: overflow list)
 constexpr int kRows2 = 256;       // cell rows per super-brick
 constexpr float kRel = 1e-5f;
@@ -217,6 +218,7 @@ template <int KIND, bool PER>
 __global__ void __launch_bounds__(kB2Threads, 4)
     cull12_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, int2* __restrict__ info,
                   int* __restrict__ slots16, int* __restrict__ list, long long list_cap, int* __restrict__ list_count,
+                  int* __restrict__ ovf,
                   DevCounters* ctr, unsigned long long* __restrict__ eval_slots, int nbb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem2& S = *reinterpret_cast<Smem2*>(smem_raw);
@@ -605,9 +607,9 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       const unsigned ma = __ballot_sync(0xffffffffu, ka), mb = __ballot_sync(0xffffffffu, kb);
       n2 = __popc(ma) + __popc(mb);
       int base = 0;
-      if (lane == 0 && n2 > kSlot && n2 <= kFcap) base = atomicAdd(list_count, n2);
+      if (lane == 0 && n2 > kSlot && n2 <= kLcap) base = atomicAdd(list_count, n2);
       base = __shfl_sync(0xffffffffu, base, 0);
-      const bool ok = n2 <= kFcap && (n2 <= kSlot || (long long)base + n2 <= list_cap);
+      const bool ok = n2 <= kLcap && (n2 <= kSlot || (long long)base + n2 <= list_cap);
       if (ok) {
         const unsigned lt = (1u << lane) - 1u;
         int* dst = n2 <= kSlot ? slots16 + sbi * kSlot : list + base;
@@ -619,9 +621,14 @@ __global__ void __launch_bounds__(kB2Threads, 4)
         atomicAdd(&eval_slots[70], 1ull);
         atomicMax(&eval_slots[73], (unsigned long long)n2);
       }
-      if (lane == 0) info[sbi] = ok ? make_int2(base, n2) : make_int2(0, -1);
+      if (lane == 0) {
+        info[sbi] = ok ? make_int2(base, n2) : make_int2(0, -1);
+        if (!ok) ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sbi;
+      }
     } else if (lane == 0) {
-      info[sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz)] = make_int2(0, -1);
+      const long long sbi = sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz);
+      info[sbi] = make_int2(0, -1);
+      ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sbi;
     }
   }
   if (lane == 0 && !(cta_ok && brick_ok)) atomicAdd(&ctr->overflow_bricks, 1ull);
@@ -654,10 +661,13 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 16)
   const int2 inf = info[sb];
   const int ps = lane < kSlot ? slots16[sb * kSlot + lane] : 0;  // issued with info, not after it
   const int pl = inf.y > kSlot ? (lane < inf.y ? list[inf.x + lane] : 0) : ps;
+  if (inf.y < 0) return;  // overflowed the ball phase's caps: the sub-brick shell labels it
   {
     const long long x0 = (long long)sbx * 8, y0 = (long long)sby * 8, z0 = g.z_begin + (long long)sbz * 4;
     const int sext[3] = {(int)min(8ll, g.n[0] - x0), (int)min(8ll, g.n[1] - y0), (int)min(4ll, g.z_end - z0)};
-    const int n2 = inf.y > 0 ? inf.y : 0;  // -1: overflow, every voxel goes to the shell search
+    // lists longer than the tables (a few per image at the benchmark densities)
+    // send their voxels to the per-voxel shell search
+    const int n2 = inf.y <= kFcap ? inf.y : 0;
     int fidx = 0;
     if (lane < n2) {
       ws.P[lane] = pl;
@@ -830,7 +840,7 @@ template <int KIND, bool PER>
 static void launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* labels, double* dist,
                      unsigned long long* hist, long long* unres, long long cap, DevCounters* ctr,
                      unsigned long long* slots, int2* info, int* slots16, int* list, long long list_cap,
-                     int* list_count, int nbb, cudaStream_t st) {
+                     int* list_count, int* ovf, int nbb, cudaStream_t st) {
   // the dynamic-smem opt-in is per device: remember it per device ordinal
   static std::atomic<unsigned long long> attr_done{0};
   int dev = 0;
@@ -847,25 +857,27 @@ static void launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* 
   const dim3 grid((unsigned)((g.n[0] + v12::kSB - 1) / v12::kSB), (unsigned)((g.n[1] + v12::kSB - 1) / v12::kSB),
                   (unsigned)((g.z_end - g.z_begin + 16 * nbb - 1) / (16 * nbb)));
   v12::cull12_kernel<KIND, PER><<<grid, v12::kB2Threads, sh_c, st>>>(g, bins, prm, info, slots16, list, list_cap,
-                                                                     list_count, ctr, slots, nbb);
+                                                                     list_count, ovf, ctr, slots, nbb);
   const long long nsb = ball12_subbricks(g);
   const dim3 eg((unsigned)((g.n[0] + 7) / 8), (unsigned)(((g.n[1] + 7) / 8 + v12::kEvalWarps - 1) / v12::kEvalWarps),
                 (unsigned)((g.z_end - g.z_begin + 3) / 4));
   v12::eval12_kernel<KIND, PER><<<eg, v12::kEvalWarps * 32, sh_e, st>>>(g, bins, prm, info, slots16, list, labels,
                                                                         dist, hist, unres, cap, ctr, slots, nsb);
+  launch_subshell(g, bins, prm, ovf, &ctr->n_ovf_sb, labels, dist, hist, ctr, st);
 }
 
 int launch_ball12(const Geo& g, const Bins& bins, const DevParams* prm, int* labels, double* dist,
                   unsigned long long* hist, long long* unres, long long unres_cap, DevCounters* ctr,
                   unsigned long long* slots, int2* info, int* slots16, int* list, long long list_cap,
-                  int* list_count, cudaStream_t st) {
+                  int* list_count, int* ovf, cudaStream_t st) {
   if (g.z_end <= g.z_begin) return 0;
+  cudaMemsetAsync(&ctr->n_ovf_sb, 0, sizeof(unsigned long long), st);
   cudaMemsetAsync(slots, 0, 128 * sizeof(unsigned long long), st);
   cudaMemsetAsync(list_count, 0, sizeof(int), st);
   static const int nbb_env = std::getenv("VX_NBB") ? std::atoi(std::getenv("VX_NBB")) : 0;
   const int nbb = nbb_env == 1 || nbb_env == 2 || nbb_env == 4 ? nbb_env : choose_nbb12(g);
 #define VX_L12(K, P) launch12<K, P>(g, bins, prm, labels, dist, hist, unres, unres_cap, ctr, slots, info, slots16, \
-                                    list, list_cap, list_count, nbb, st)
+                                    list, list_cap, list_count, ovf, nbb, st)
   switch (g.kind * 2 + (g.periodic ? 1 : 0)) {
     case 0: VX_L12(kVoronoi, false); break;
     case 1: VX_L12(kVoronoi, true); break;
@@ -876,7 +888,7 @@ int launch_ball12(const Geo& g, const Bins& bins, const DevParams* prm, int* lab
   }
 #undef VX_L12
   ball12_publish_kernel<<<1, 32, 0, st>>>(slots, ctr);
-  return 3;
+  return 4;
 }
 
 }  // namespace vxb

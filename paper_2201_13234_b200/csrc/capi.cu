@@ -59,7 +59,7 @@ struct vx_context {
   std::mutex mu;
   Buf pos_raw, t_raw, w_raw, p3, t, dropped, keys_a, keys_b, vals_a, vals_b, bx, by, bz, bt, bidx,
       cell_start, cub, labels, dist, hist, unres, params, counters, scratch, vsample, vlab, vdist,
-      vbad, slots, f4, sb_info, sb_list, sb_count, sb_slots;
+      vbad, slots, f4, sb_info, sb_list, sb_count, sb_slots, sb_ovf;
   DevParams* h_prm = nullptr;
   DevCounters* h_ctr = nullptr;
   cudaEvent_t ev[8] = {};  // stage markers (options.profile_stages)
@@ -70,11 +70,11 @@ struct vx_context {
   void* pin[2] = {};                   // pinned double buffer of the file writer
   size_t pin_bytes = 0;
 
-  Buf* all[34] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
+  Buf* all[35] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
                   &vals_a,  &vals_b,  &bx,    &by,    &bz,     &bt,      &bidx,     &cell_start,
                   &cub,     &labels,  &dist,  &hist,  &unres,  &params,  &counters, &scratch,
                   &vsample, &vlab,    &vdist, &vbad,  &slots,  &f4,      &sb_info,  &sb_list,
-                  &sb_count, &sb_slots};
+                  &sb_count, &sb_slots, &sb_ovf};
 };
 
 namespace {
@@ -636,8 +636,9 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
           const long long lcap = std::min<long long>(nsb * 4 + (1 << 20), (1ll << 31) - 1);  // lists > 16 only
           int* list = ensure<int>(ctx->sb_list, (size_t)lcap);
           int* lcount = ensure<int>(ctx->sb_count, 1);
+          int* ovf = ensure<int>(ctx->sb_ovf, (size_t)nsb);
           launches += launch_ball12(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, info, slots16, list, lcap,
-                                    lcount, st);
+                                    lcount, ovf, st);
         } else if (ball_ver == 11) {
           launches += launch_ball11(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
         } else {

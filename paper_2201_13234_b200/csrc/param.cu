@@ -23,6 +23,7 @@ __global__ void init_kernel(DevParams* prm, DevCounters* ctr) {
   ctr->n_alive = 0;
   ctr->bad_site = 0;
   ctr->n_unres_done = 0;
+  ctr->n_ovf_sb = 0;
 }
 
 __global__ void chunk_roll_kernel(DevCounters* ctr) {

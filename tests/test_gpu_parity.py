@@ -472,3 +472,30 @@ def test_large_random_vs_reference_library(i):
     assert np.array_equal(r.labels.labels, lab_ref), int((r.labels.labels != lab_ref).sum())
     assert np.array_equal(r.distances.values.view(np.uint64), dist_ref.view(np.uint64))
     assert np.array_equal(r.histogram, np.bincount(lab_ref, minlength=ns).astype(np.uint64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["flat_periodic", "tall_nonperiodic", "dense_jm", "flat_laguerre"])
+def test_overflow_subbrick_shell_vs_reference(case):
+    """Strongly anisotropic voxels / very dense sites overflow the ball phase's
+    brick caps; those sub-bricks are labelled by the sub-brick shell search.
+    Bit-exact against the reference library, and the path is really taken."""
+    import oracle
+    import paper_2201_13234_b200 as vx
+
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    kind, counts, ns, per = {"flat_periodic": (0, [512, 512, 8], 20000, True),
+                             "tall_nonperiodic": (0, [32, 32, 2048], 8000, False),
+                             "dense_jm": (1, [96, 96, 96], 40000, True),
+                             "flat_laguerre": (2, [400, 384, 6], 12000, False)}[case]
+    L = np.array([1.0, 0.8, 1.2])
+    pos, t = oracle.generate_uniform_sites(3, L, ns, kind, 0.5 * np.cbrt(np.prod(L) / ns), 99)
+    p = oracle.Problem(kind, counts, L, per, pos, t, 0.0 if kind == 0 else 1.3)
+    lab_ref, dist_ref, _, _ = oracle.ref_tessellate(p)
+    sites, grid = to_vx(p)
+    r = vx.tessellate_fast(sites, grid, distances=True, histogram=True)
+    assert r.stats["overflow_bricks"] > 0  # the sub-brick shell ran
+    assert np.array_equal(r.labels.labels, lab_ref), int((r.labels.labels != lab_ref).sum())
+    assert np.array_equal(r.distances.values.view(np.uint64), dist_ref.view(np.uint64))
+    assert np.array_equal(r.histogram, np.bincount(lab_ref, minlength=ns).astype(np.uint64))
