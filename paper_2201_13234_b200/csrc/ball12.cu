@@ -71,6 +71,10 @@ constexpr int kTcap = 512;        // sites kept per super-brick (else the CTA fa
 constexpr int kWcap = 64;         // brick-level survivors per warp (2 slots per lane)
 constexpr int kFcap = 32;         // sub-brick survivors the eval kernel evaluates
 constexpr int kLcap = 64;         // sub-brick list capacity (<= the brick list's kWcap)
+// dense mode (site spacing below ~8.5 voxels, chosen on the host): longer
+// brick lists, a two-pass chunked sub-brick cull and a chunked eval
+constexpr int kWcapD = 256;
+constexpr int kLcapD = 128;
 constexpr int kSlot = 16;         // fixed list slots per sub-brick (longer lists: overflow list)
 constexpr int kRows2 = 256;       // cell rows per super-brick
 constexpr float kRel = 1e-5f;
@@ -81,17 +85,20 @@ struct FBox {
 };
 
 struct __align__(16) WarpSmem {
-  int W[kWcap];        // brick list (gather slots), ascending site index
+  int W[kWcapD];       // brick list (gather slots), ascending site index
+  int L[kLcapD];       // dense mode: a sub-brick's survivors (binned positions)
 };
 
-// eval12: per warp (one sub-brick)
-struct __align__(16) EvalSmem {
-  double T[kFcap][20]; // exact w^2: [0,8) x, [8,16) y, [16,20) z
-  double Ft[kFcap];
-  int P[kFcap];        // binned positions
-  int Fidx[kFcap];
-  int cnt[kFcap];
+// eval12: per warp (one sub-brick); LC = list capacity
+template <int LC>
+struct __align__(16) EvalSmemT {
+  double T[kFcap][20]; // exact w^2 of one pass of kFcap candidates: [0,8) x, [8,16) y, [16,20) z
+  double Ft[LC];
+  int P[LC];           // binned positions
+  int Fidx[LC];
+  int cnt[LC];
 };
+using EvalSmem = EvalSmemT<kFcap>;
 
 struct Smem2 {
   float4 rel[kTcap];   // (ux, uy, uz, t) relative to the super-brick centre
@@ -214,7 +221,7 @@ __device__ __forceinline__ long long wrapi2(long long c, long long m) {
   return r < 0 ? r + m : r;
 }
 
-template <int KIND, bool PER>
+template <int KIND, bool PER, bool DENSE>
 __global__ void __launch_bounds__(kB2Threads, 4)
     cull12_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, int2* __restrict__ info,
                   int* __restrict__ slots16, int* __restrict__ list, long long list_cap, int* __restrict__ list_count,
@@ -546,10 +553,10 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       const bool keep = f0 + lane < T && ((S.mk[wid][f] >> bb) & 1u);
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       const int pos = nW + __popc(m & ((1u << lane) - 1u));
-      if (keep && pos < kWcap) ws.W[pos] = f;  // ballot order = ord order = site order
+      if (keep && pos < (DENSE ? kWcapD : kWcap)) ws.W[pos] = f;  // ballot order = ord order = site order
       nW += __popc(m);
     }
-    brick_ok = nW <= kWcap;
+    brick_ok = nW <= (DENSE ? kWcapD : kWcap);
     if (VX_STATS_ON && lane == 0) {
       atomicAdd(&eval_slots[67], (unsigned long long)nW);
       atomicAdd(&eval_slots[68], 1ull);
@@ -563,7 +570,70 @@ __global__ void __launch_bounds__(kB2Threads, 4)
     const int sext[3] = {bext[0], bext[1], min(4, ext[2] - sz)};
     if (sext[1] <= 0 || sext[2] <= 0) continue;
     int n2 = 0;
-    if (brick_ok) {
+    if (DENSE && brick_ok) {
+      // two passes over the brick list in chunks of 32: arg-min of the upper
+      // bounds (the reference s0), then tau + bisector cull and compaction in
+      // slot (= site index) order
+      const FBox Bs = box_of(bxo, sy, sz, sext[0], sext[1], sext[2]);
+      auto okey = [](float v) -> unsigned {
+        const unsigned b = __float_as_uint(v);
+        return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+      };
+      unsigned km = 0xffffffffu;
+      for (int c0 = 0; c0 < nW; c0 += 32) {
+        const int k = c0 + lane;
+        if (k < nW) {
+          const int f = ws.W[k];
+          SiteF t;
+          fbounds<KIND, PER>(S.rel[f], S.flag[f], Bs, halfLf, invG, t);
+          km = min(km, (okey(t.ubp) & ~255u) | (unsigned)k);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) km = min(km, __shfl_xor_sync(0xffffffffu, km, o));
+      const int r0 = (int)(km & 255u);
+      const int fr = ws.W[r0];
+      const unsigned fl0 = S.flag[fr];
+      SiteF z;  // every lane derives the reference's bounds itself
+      fbounds<KIND, PER>(S.rel[fr], fl0, Bs, halfLf, invG, z);
+      const float tau = z.ubp;  // >= the minimum upper bound: a valid cull level
+      for (int c0 = 0; c0 < nW; c0 += 32) {
+        const int k = c0 + lane;
+        bool keep = false;
+        int f = 0;
+        if (k < nW) {
+          f = ws.W[k];
+          const unsigned fl = S.flag[f];
+          SiteF t;
+          fbounds<KIND, PER>(S.rel[f], fl, Bs, halfLf, invG, t);
+          keep = k == r0 || (t.lbp <= tau && bisector_keep<KIND, PER>(t, fl, z, fl0, Bs, halfLf, invG, e_d));
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        const int pos = n2 + __popc(m & ((1u << lane) - 1u));
+        if (keep && pos < kLcapD) ws.L[pos] = S.p[f];
+        n2 += __popc(m);
+      }
+      __syncwarp();
+      const long long sbi = sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz);
+      int base = 0;
+      if (lane == 0 && n2 > kSlot && n2 <= kLcapD) base = atomicAdd(list_count, n2);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const bool ok = n2 <= kLcapD && (n2 <= kSlot || (long long)base + n2 <= list_cap);
+      if (ok) {
+        int* dst = n2 <= kSlot ? slots16 + sbi * kSlot : list + base;
+        for (int i = lane; i < n2; i += 32) dst[i] = ws.L[i];
+      }
+      __syncwarp();
+      if (VX_STATS_ON && lane == 0) {
+        atomicAdd(&eval_slots[69], (unsigned long long)n2);
+        atomicAdd(&eval_slots[70], 1ull);
+        atomicMax(&eval_slots[73], (unsigned long long)n2);
+      }
+      if (lane == 0) {
+        info[sbi] = ok ? make_int2(base, n2) : make_int2(0, -1);
+        if (!ok) ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sbi;
+      }
+    } else if (brick_ok) {
       const FBox Bs = box_of(bxo, sy, sz, sext[0], sext[1], sext[2]);
       // one bound evaluation per brick-list site, kept in registers (slots
       // lane and lane + 32; nW <= 64)
@@ -640,7 +710,7 @@ constexpr int kEvalWarps = 2;  // sub-bricks along y per CTA
 // One warp per 8x8x4 sub-brick (the tail of v11's sub-brick loop: exact
 // tables, evaluation, stores, histogram, unresolved compaction).  The site
 // index load is issued before the tables and consumed at the store.
-template <int KIND, bool PER>
+template <int KIND, bool PER, bool DENSE>
 __global__ void __launch_bounds__(kEvalWarps * 32, 16)
     eval12_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, const int2* __restrict__ info,
                   const int* __restrict__ slots16, const int* __restrict__ list, int* __restrict__ labels,
@@ -649,7 +719,8 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 16)
                   DevCounters* ctr, unsigned long long* __restrict__ eval_slots, long long nsb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  EvalSmem& ws = reinterpret_cast<EvalSmem*>(smem_raw)[wid];
+  using ES = EvalSmemT<DENSE ? kLcapD : kFcap>;
+  ES& ws = reinterpret_cast<ES*>(smem_raw)[wid];
   const unsigned nsbx = (unsigned)((g.n[0] + 7) / 8), nsby = (unsigned)((g.n[1] + 7) / 8);
   const double cutoff = prm->cutoff;
   const long long slab_base = g.z_begin * g.n[0] * g.n[1];
@@ -667,67 +738,30 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 16)
     const int sext[3] = {(int)min(8ll, g.n[0] - x0), (int)min(8ll, g.n[1] - y0), (int)min(4ll, g.z_end - z0)};
     // lists longer than the tables (a few per image at the benchmark densities)
     // send their voxels to the per-voxel shell search
-    const int n2 = inf.y <= kFcap ? inf.y : 0;
+    const int n2 = inf.y <= (DENSE ? kLcapD : kFcap) ? inf.y : 0;
     int fidx = 0;
-    if (lane < n2) {
-      ws.P[lane] = pl;
-      ws.cnt[lane] = 0;
-      fidx = bins.idx[pl];
-      if (KIND != kVoronoi) ws.Ft[lane] = bins.t[pl];
-    }
-    __syncwarp();
-    // exact per-axis tables (the reference arithmetic): one lane per (site, axis)
-    for (int e = lane; e < 3 * n2; e += 32) {
-      const int a = e >= 2 * n2 ? 2 : (e >= n2 ? 1 : 0);
-      const int j = e - a * n2;
-      const int p = ws.P[j];
-      const double sv = a == 0 ? bins.x[p] : (a == 1 ? bins.y[p] : bins.z[p]);
-      const long long k0 = a == 0 ? x0 : (a == 1 ? y0 : z0);
-      const double spa = a == 0 ? g.sp[0] : (a == 1 ? g.sp[1] : g.sp[2]);
-      const double La = a == 0 ? g.L[0] : (a == 1 ? g.L[1] : g.L[2]);
-      const double iLa = a == 0 ? g.invL[0] : (a == 1 ? g.invL[1] : g.invL[2]);
-      const double lim = 0.49 * La;
-      double* trow = &ws.T[j][a * 8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        if (a == 2 && r >= 4) break;
-        const double u = __dsub_rn(sv, center(k0 + r, spa));  // geometry.hpp:58-60
-        // |u| < 0.49 L: floor(u*invL + 0.5) == 0, so the reference's wrap is u itself
-        const double w = (!PER || fabs(u) < lim) ? u : wrap_delta(u, La, iLa);
-        trow[r] = __dmul_rn(w, w);
+    if constexpr (DENSE) {
+      for (int i = lane; i < n2; i += 32) {
+        const int p = n2 <= kSlot ? slots16[sb * kSlot + i] : list[inf.x + i];
+        ws.P[i] = p;
+        ws.cnt[i] = 0;
+        ws.Fidx[i] = bins.idx[p];
+        if (KIND != kVoronoi) ws.Ft[i] = bins.t[p];
+      }
+    } else {
+      if (lane < n2) {
+        ws.P[lane] = pl;
+        ws.cnt[lane] = 0;
+        fidx = bins.idx[pl];
+        if (KIND != kVoronoi) ws.Ft[lane] = bins.t[pl];
       }
     }
     __syncwarp();
-    // exact evaluation: lane -> 4 voxels along x in rows vy and vy + 4
-    double best[8];
-    int bj[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      best[k] = __longlong_as_double(0x7ff0000000000000ll);
-      bj[k] = -1;
-    }
-    const bool g1 = g.g_is_one;
-    for (int j = 0; j < n2; ++j) {
-      const double wz = ws.T[j][16 + vz];
-      const double a0 = __dadd_rn(wz, ws.T[j][8 + vy]);  // 0 + wz^2 == wz^2
-      const double a1 = __dadd_rn(wz, ws.T[j][12 + vy]);
-      const double2 w01 = *reinterpret_cast<const double2*>(&ws.T[j][qx]);
-      const double2 w23 = *reinterpret_cast<const double2*>(&ws.T[j][qx + 2]);
-      const double tj = KIND == kVoronoi ? 0.0 : ws.Ft[j];
-      const double d[8] = {__dadd_rn(a0, w01.x), __dadd_rn(a0, w01.y), __dadd_rn(a0, w23.x),
-                           __dadd_rn(a0, w23.y), __dadd_rn(a1, w01.x), __dadd_rn(a1, w01.y),
-                           __dadd_rn(a1, w23.x), __dadd_rn(a1, w23.y)};
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const double pr = prox_from_dsq<KIND>(d[k], g.growth, g1, tj);
-        if (pr < best[k]) {
-          best[k] = pr;
-          bj[k] = j;
-        }
-      }
-    }
+    auto store_tail = [&](double (&best)[8], int (&bj)[8]) {
     // resolve + store + compaction of unresolved voxels
-    if (lane < n2) ws.Fidx[lane] = fidx;  // its load was issued before the tables
+    if constexpr (!DENSE) {
+      if (lane < n2) ws.Fidx[lane] = fidx;  // its load was issued before the tables
+    }
     __syncwarp();
 
     const long long kz = z0 + vz;
@@ -792,7 +826,120 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 16)
       atomicAdd(&eval_slots[sb & 63], (unsigned long long)n2 * (sext[0] * sext[1] * sext[2]));
     if (hist && n2 > 0) {
       __syncwarp();
-      if (lane < n2 && ws.cnt[lane]) atomicAdd(&hist[ws.Fidx[lane]], (unsigned long long)ws.cnt[lane]);
+      for (int i = lane; i < (DENSE ? n2 : min(n2, 32)); i += 32)
+        if (ws.cnt[i]) atomicAdd(&hist[ws.Fidx[i]], (unsigned long long)ws.cnt[i]);
+    }
+    };
+    if constexpr (DENSE) {
+      double best[8];
+      int bj[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        best[k] = __longlong_as_double(0x7ff0000000000000ll);
+        bj[k] = -1;
+      }
+      const bool g1 = g.g_is_one;
+      // candidates in passes of kFcap tables; the running minimum carries
+      // over, so the scan order is still ascending site index
+      for (int c0 = 0; c0 < n2; c0 += kFcap) {
+        const int m = min(kFcap, n2 - c0);
+    // exact per-axis tables (the reference arithmetic): one lane per (site, axis)
+    for (int e = lane; e < 3 * m; e += 32) {
+      const int a = e >= 2 * m ? 2 : (e >= m ? 1 : 0);
+      const int j = e - a * m;
+      const int p = ws.P[c0 + j];
+      const double sv = a == 0 ? bins.x[p] : (a == 1 ? bins.y[p] : bins.z[p]);
+      const long long k0 = a == 0 ? x0 : (a == 1 ? y0 : z0);
+      const double spa = a == 0 ? g.sp[0] : (a == 1 ? g.sp[1] : g.sp[2]);
+      const double La = a == 0 ? g.L[0] : (a == 1 ? g.L[1] : g.L[2]);
+      const double iLa = a == 0 ? g.invL[0] : (a == 1 ? g.invL[1] : g.invL[2]);
+      const double lim = 0.49 * La;
+      double* trow = &ws.T[j][a * 8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        if (a == 2 && r >= 4) break;
+        const double u = __dsub_rn(sv, center(k0 + r, spa));  // geometry.hpp:58-60
+        // |u| < 0.49 L: floor(u*invL + 0.5) == 0, so the reference's wrap is u itself
+        const double w = (!PER || fabs(u) < lim) ? u : wrap_delta(u, La, iLa);
+        trow[r] = __dmul_rn(w, w);
+      }
+    }
+    __syncwarp();
+    // exact evaluation: lane -> 4 voxels along x in rows vy and vy + 4
+    for (int j = 0; j < m; ++j) {
+      const double wz = ws.T[j][16 + vz];
+      const double a0 = __dadd_rn(wz, ws.T[j][8 + vy]);  // 0 + wz^2 == wz^2
+      const double a1 = __dadd_rn(wz, ws.T[j][12 + vy]);
+      const double2 w01 = *reinterpret_cast<const double2*>(&ws.T[j][qx]);
+      const double2 w23 = *reinterpret_cast<const double2*>(&ws.T[j][qx + 2]);
+      const double tj = KIND == kVoronoi ? 0.0 : ws.Ft[c0 + j];
+      const double d[8] = {__dadd_rn(a0, w01.x), __dadd_rn(a0, w01.y), __dadd_rn(a0, w23.x),
+                           __dadd_rn(a0, w23.y), __dadd_rn(a1, w01.x), __dadd_rn(a1, w01.y),
+                           __dadd_rn(a1, w23.x), __dadd_rn(a1, w23.y)};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double pr = prox_from_dsq<KIND>(d[k], g.growth, g1, tj);
+        if (pr < best[k]) {
+          best[k] = pr;
+          bj[k] = c0 + j;
+        }
+      }
+    }
+        __syncwarp();  // the next pass rewrites the tables
+      }
+      store_tail(best, bj);
+    } else {
+    // exact per-axis tables (the reference arithmetic): one lane per (site, axis)
+    for (int e = lane; e < 3 * n2; e += 32) {
+      const int a = e >= 2 * n2 ? 2 : (e >= n2 ? 1 : 0);
+      const int j = e - a * n2;
+      const int p = ws.P[j];
+      const double sv = a == 0 ? bins.x[p] : (a == 1 ? bins.y[p] : bins.z[p]);
+      const long long k0 = a == 0 ? x0 : (a == 1 ? y0 : z0);
+      const double spa = a == 0 ? g.sp[0] : (a == 1 ? g.sp[1] : g.sp[2]);
+      const double La = a == 0 ? g.L[0] : (a == 1 ? g.L[1] : g.L[2]);
+      const double iLa = a == 0 ? g.invL[0] : (a == 1 ? g.invL[1] : g.invL[2]);
+      const double lim = 0.49 * La;
+      double* trow = &ws.T[j][a * 8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        if (a == 2 && r >= 4) break;
+        const double u = __dsub_rn(sv, center(k0 + r, spa));  // geometry.hpp:58-60
+        // |u| < 0.49 L: floor(u*invL + 0.5) == 0, so the reference's wrap is u itself
+        const double w = (!PER || fabs(u) < lim) ? u : wrap_delta(u, La, iLa);
+        trow[r] = __dmul_rn(w, w);
+      }
+    }
+    __syncwarp();
+    // exact evaluation: lane -> 4 voxels along x in rows vy and vy + 4
+    double best[8];
+    int bj[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      best[k] = __longlong_as_double(0x7ff0000000000000ll);
+      bj[k] = -1;
+    }
+    const bool g1 = g.g_is_one;
+    for (int j = 0; j < n2; ++j) {
+      const double wz = ws.T[j][16 + vz];
+      const double a0 = __dadd_rn(wz, ws.T[j][8 + vy]);  // 0 + wz^2 == wz^2
+      const double a1 = __dadd_rn(wz, ws.T[j][12 + vy]);
+      const double2 w01 = *reinterpret_cast<const double2*>(&ws.T[j][qx]);
+      const double2 w23 = *reinterpret_cast<const double2*>(&ws.T[j][qx + 2]);
+      const double tj = KIND == kVoronoi ? 0.0 : ws.Ft[j];
+      const double d[8] = {__dadd_rn(a0, w01.x), __dadd_rn(a0, w01.y), __dadd_rn(a0, w23.x),
+                           __dadd_rn(a0, w23.y), __dadd_rn(a1, w01.x), __dadd_rn(a1, w01.y),
+                           __dadd_rn(a1, w23.x), __dadd_rn(a1, w23.y)};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double pr = prox_from_dsq<KIND>(d[k], g.growth, g1, tj);
+        if (pr < best[k]) {
+          best[k] = pr;
+          bj[k] = j;
+        }
+      }
+    }
+      store_tail(best, bj);
     }
   }
 }
@@ -836,7 +983,19 @@ long long ball12_subbricks(const Geo& g) {
   return ((g.n[0] + 7) / 8) * ((g.n[1] + 7) / 8) * ((g.z_end - g.z_begin + 3) / 4);
 }
 
-template <int KIND, bool PER>
+// Dense mode when the mean site spacing is below ~8.5 voxels (on the finest
+// true axis): an 8^3 brick then sees more than ~60 sites (VX_DENSE=0/1 forces).
+bool ball12_dense(const Geo& g) {
+  static const int env = std::getenv("VX_DENSE") ? std::atoi(std::getenv("VX_DENSE")) : -1;
+  if (env == 0 || env == 1) return env == 1;
+  double sp = 1e300;
+  for (int a = 0; a < 3; ++a)
+    if (g.n[a] > 1) sp = std::min(sp, g.sp[a]);
+  const double spacing = pow(g.vol_true / (double)(g.n_sites > 0 ? g.n_sites : 1), 1.0 / g.dim);
+  return sp < 1e300 && spacing < 8.5 * sp;
+}
+
+template <int KIND, bool PER, bool DENSE>
 static void launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* labels, double* dist,
                      unsigned long long* hist, long long* unres, long long cap, DevCounters* ctr,
                      unsigned long long* slots, int2* info, int* slots16, int* list, long long list_cap,
@@ -848,20 +1007,20 @@ static void launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* 
   const unsigned long long bit = 1ull << (dev & 63);
   const bool attr = (attr_done.load() & bit) != 0;
   const size_t sh_c = sizeof(v12::Smem2);
-  const size_t sh_e = sizeof(v12::EvalSmem) * v12::kEvalWarps;
+  const size_t sh_e = sizeof(v12::EvalSmemT<DENSE ? v12::kLcapD : v12::kFcap>) * v12::kEvalWarps;
   if (!attr) {
-    cudaFuncSetAttribute(v12::cull12_kernel<KIND, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_c);
-    cudaFuncSetAttribute(v12::eval12_kernel<KIND, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_e);
+    cudaFuncSetAttribute(v12::cull12_kernel<KIND, PER, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_c);
+    cudaFuncSetAttribute(v12::eval12_kernel<KIND, PER, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_e);
     attr_done.fetch_or(bit);
   }
   const dim3 grid((unsigned)((g.n[0] + v12::kSB - 1) / v12::kSB), (unsigned)((g.n[1] + v12::kSB - 1) / v12::kSB),
                   (unsigned)((g.z_end - g.z_begin + 16 * nbb - 1) / (16 * nbb)));
-  v12::cull12_kernel<KIND, PER><<<grid, v12::kB2Threads, sh_c, st>>>(g, bins, prm, info, slots16, list, list_cap,
+  v12::cull12_kernel<KIND, PER, DENSE><<<grid, v12::kB2Threads, sh_c, st>>>(g, bins, prm, info, slots16, list, list_cap,
                                                                      list_count, ovf, ctr, slots, nbb);
   const long long nsb = ball12_subbricks(g);
   const dim3 eg((unsigned)((g.n[0] + 7) / 8), (unsigned)(((g.n[1] + 7) / 8 + v12::kEvalWarps - 1) / v12::kEvalWarps),
                 (unsigned)((g.z_end - g.z_begin + 3) / 4));
-  v12::eval12_kernel<KIND, PER><<<eg, v12::kEvalWarps * 32, sh_e, st>>>(g, bins, prm, info, slots16, list, labels,
+  v12::eval12_kernel<KIND, PER, DENSE><<<eg, v12::kEvalWarps * 32, sh_e, st>>>(g, bins, prm, info, slots16, list, labels,
                                                                         dist, hist, unres, cap, ctr, slots, nsb);
   launch_subshell(g, bins, prm, ovf, &ctr->n_ovf_sb, labels, dist, hist, ctr, st);
 }
@@ -876,8 +1035,12 @@ int launch_ball12(const Geo& g, const Bins& bins, const DevParams* prm, int* lab
   cudaMemsetAsync(list_count, 0, sizeof(int), st);
   static const int nbb_env = std::getenv("VX_NBB") ? std::atoi(std::getenv("VX_NBB")) : 0;
   const int nbb = nbb_env == 1 || nbb_env == 2 || nbb_env == 4 ? nbb_env : choose_nbb12(g);
-#define VX_L12(K, P) launch12<K, P>(g, bins, prm, labels, dist, hist, unres, unres_cap, ctr, slots, info, slots16, \
-                                    list, list_cap, list_count, ovf, nbb, st)
+  const bool dense = ball12_dense(g);
+#define VX_L12(K, P)                                                                                          \
+  (dense ? launch12<K, P, true>(g, bins, prm, labels, dist, hist, unres, unres_cap, ctr, slots, info, slots16, \
+                                list, list_cap, list_count, ovf, nbb, st)                                     \
+         : launch12<K, P, false>(g, bins, prm, labels, dist, hist, unres, unres_cap, ctr, slots, info, slots16, \
+                                 list, list_cap, list_count, ovf, nbb, st))
   switch (g.kind * 2 + (g.periodic ? 1 : 0)) {
     case 0: VX_L12(kVoronoi, false); break;
     case 1: VX_L12(kVoronoi, true); break;

@@ -633,7 +633,8 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
           const long long nsb = ball12_subbricks(gg);
           int2* info = ensure<int2>(ctx->sb_info, (size_t)nsb);
           int* slots16 = ensure<int>(ctx->sb_slots, (size_t)nsb * 16);
-          const long long lcap = std::min<long long>(nsb * 4 + (1 << 20), (1ll << 31) - 1);  // lists > 16 only
+          const long long lcap =  // lists > 16 only (dense mode: most of them)
+              std::min<long long>(nsb * (ball12_dense(gg) ? 48 : 4) + (1 << 20), (1ll << 31) - 1);
           int* list = ensure<int>(ctx->sb_list, (size_t)lcap);
           int* lcount = ensure<int>(ctx->sb_count, 1);
           int* ovf = ensure<int>(ctx->sb_ovf, (size_t)nsb);

@@ -499,3 +499,25 @@ def test_overflow_subbrick_shell_vs_reference(case):
     assert np.array_equal(r.labels.labels, lab_ref), int((r.labels.labels != lab_ref).sum())
     assert np.array_equal(r.distances.values.view(np.uint64), dist_ref.view(np.uint64))
     assert np.array_equal(r.histogram, np.bincount(lab_ref, minlength=ns).astype(np.uint64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,per", [(0, True), (0, False), (1, True), (2, True)])
+def test_dense_mode_vs_reference(kind, per):
+    """Site spacing below ~8.5 voxels selects the dense ball path (long brick
+    lists, chunked cull and eval); bit-exact against the reference library."""
+    import oracle
+    import paper_2201_13234_b200 as vx
+
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    counts, ns = [120, 112, 128], 24000  # spacing ~4.3 voxels
+    L = np.array([1.0, 0.93, 1.07])
+    pos, t = oracle.generate_uniform_sites(3, L, ns, kind, 0.5 * np.cbrt(np.prod(L) / ns), 5 + kind)
+    p = oracle.Problem(kind, counts, L, per, pos, t, 0.0 if kind == 0 else 0.9)
+    lab_ref, dist_ref, _, _ = oracle.ref_tessellate(p)
+    sites, grid = to_vx(p)
+    r = vx.tessellate_fast(sites, grid, distances=True, histogram=True)
+    assert np.array_equal(r.labels.labels, lab_ref), int((r.labels.labels != lab_ref).sum())
+    assert np.array_equal(r.distances.values.view(np.uint64), dist_ref.view(np.uint64))
+    assert np.array_equal(r.histogram, np.bincount(lab_ref, minlength=ns).astype(np.uint64))
