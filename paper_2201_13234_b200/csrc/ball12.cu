@@ -1,55 +1,41 @@
-// K2 (v12): the ball phase of v11 split in two kernels.
+// K2 (v12, default): the ball phase of tessellate_fast in gather form
+// (reference step 1, tessellate.cpp:103-144 + ball_scan.hpp:55-124), as two
+// kernels.
 //
-//   cull12  : v11's gather, column tau/mask passes, brick lists and sub-brick
-//             tau + bisector culls; each 8x8x4 sub-brick's survivors (binned
-//             positions, in ascending site index) go to a global list, with
-//             (offset, count) per sub-brick (count -1: overflow, the eval
-//             kernel sends every voxel of it to the shell search).
-//   eval12  : one warp per sub-brick: the exact per-axis f64 tables, the exact
-//             evaluation of 8 voxels per lane, label / distance stores, the
-//             histogram counts and the unresolved compaction.
-// Each kernel needs fewer registers and much less shared memory than the
-// fused v11, so both run at higher occupancy; the lists cost ~9 ints per
-// sub-brick of HBM traffic.
+// Contract (as ball.cu): labels/values bit-identical to the reference, because
+// every culled site loses strictly -- by far more than f64 rounding -- at every
+// voxel of the box it was culled for, and the survivors are evaluated with the
+// reference's exact f64 fold in ascending site order.  f32 bounds are widened
+// by kRel (1e-5) of their terms' magnitude plus an absolute coordinate slack
+// e_d; float rounding is ~1e-7 relative.
 //
-// v11 (below, unchanged up to the sub-brick cull):
-//
-// v11 = v10 with the brick-level tau and list passes merged over the warp's
-// column of bricks: one pass computes the upper bounds of every gathered site
-// for all (up to 4) bricks of the column at once (the x/y terms are shared),
-// one pass the lower bounds and a per-site keep mask; each brick's list is then
-// a ballot over the mask bits in site-index order.  The column height (1, 2 or
-// 4 bricks) is chosen by the host from the site density so that the gathered
-// list fits kTcap.
-//
-// v10 = v8 with 8x8x4 sub-bricks (two per brick, 8 voxels per lane in two
-// y-rows that share the x tables) and the brick list sorted by site index once
-// per brick, so each sub-brick's ballot-compacted survivors are already in the
-// reference's ascending order.  Per-sub-brick overhead (cull, tables, store) is
-// spread over 256 voxels instead of 128.
-//
-// Same contract as ball.cu (see its header): labels/values bit-identical to
-// the reference because every culled site loses strictly, by far more than
-// f64 rounding, at every voxel of the box it was culled for, and the survivors
-// are evaluated with the reference's exact f64 fold in ascending site order.
-//
-// Work split (one CTA = 8 warps = a 16^3 "super-brick"):
-//   G (CTA)  : x-rows of cells within R of the super-brick -> gathered site
-//              list in shared memory (f32 coordinates relative to the super-
-//              brick centre + time, plus the binned index); one barrier.
-//   W (warp) : each warp owns an 8^3 brick: tau = min over gathered sites of
-//              an upper bound of prox over the brick; keep sites whose lower
-//              bound is <= tau  (f32, outward-rounded margins).
-//   S (warp) : for each of the brick's four 8x4x4 sub-bricks: the same tau
-//              cull on the brick list plus the bisector test against the
-//              sub-brick's tau site s0 -> a handful of survivors, sorted by
-//              site index, exact per-axis f64 tables (ball_scan.hpp:89-96),
-//              exact evaluation of 4 voxels per lane, resolve (prox <= cutoff),
-//              int4 label stores, warp-aggregated unresolved push and
-//              per-candidate histogram counts.
-// f32 bounds: every bound is widened by kRel (1e-5) relative to the magnitude
-// of its terms plus an absolute coordinate slack e_d; float rounding is ~1e-7
-// relative, so a site is only culled if it loses by >> f64 rounding.
+// cull12 (CTA = 8 warps = a 16 x 16 x 16nbb super-brick; nbb = 1, 2 or 4 chosen
+// by the host from the site density and, for periodic z, the period):
+//   gather : x-rows of cells within R of the super-brick -> shared memory
+//            (f32 coordinates relative to the super-brick centre, time, binned
+//            position, periodic-ambiguity flags); sites that cannot reach any
+//            voxel within the cutoff are dropped; the kept sites are
+//            rank-sorted by site index once.
+//   column : each warp owns a column of nbb 8^3 bricks: one pass computes every
+//            site's upper bound of prox for all bricks of the column (the x/y
+//            terms are shared) -> per-brick tau; a second pass the lower bounds
+//            -> a per-site keep mask; each brick's list is a ballot over its
+//            mask bit, in site-index order.
+//   sub-brick : per 8 x 8 x 4 sub-brick, tau + bisector cull against the site
+//            with the least upper bound -> the survivors' binned positions, in
+//            site order, into 16 fixed slots (longer lists: an overflow list),
+//            (offset, count) per sub-brick.  Dense mode (spacing < ~8.5
+//            voxels) allows brick lists of 256 and sub-brick lists of 128 with a
+//            two-pass chunked cull.  Sub-bricks over every cap are listed for
+//            the sub-brick shell (subshell.cu).
+// eval12 (warp = one 8 x 8 x 4 sub-brick, 3-D grid): exact per-axis f64 tables
+//   (one lane per (site, axis)), exact evaluation of 8 voxels per lane in two
+//   y-rows sharing the x table (dense mode: in passes of 32 candidates),
+//   resolve (prox <= cutoff), int4 label stores, optional exact distances,
+//   per-candidate histogram counts, warp-aggregated compaction of unresolved
+//   voxels for the shell search (shell.cu).
+// Split at the sub-brick lists, both kernels fit 64 registers and run at 4
+// CTAs/SM; the lists cost ~0.7 GB of HBM traffic at cfg5.
 #include <algorithm>
 #include <atomic>
 #include <cmath>
