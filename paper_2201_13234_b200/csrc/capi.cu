@@ -52,6 +52,7 @@ struct Buf {
 }  // namespace
 
 constexpr int kMaxChunks = 16;
+constexpr int64_t kMaxZPlanes = 4095 * 64;  // gridDim.z limit x the deepest ball super-brick
 
 struct vx_context {
   int device = 0;
@@ -662,12 +663,16 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
         nchunk = e ? std::max(1, std::min(kMaxChunks, std::atoi(e))) : (nz >= 256 ? 8 : 1);
       }
       int64_t cz = nchunk > 1 ? ((nz + nchunk - 1) / nchunk + 63) / 64 * 64 : nz;
+      const bool pipelined = nchunk > 1;  // chunk D2H overlaps the next chunk's compute
       if (sink) {  // file output: chunks of <= sink_chunk_bytes() per array, whole super-bricks
         cz = std::max<int64_t>(1, sink_chunk_bytes() / (plane * (dist ? 8 : 4)));
         if (cz >= 64) cz = cz / 64 * 64;
         cz = std::min<int64_t>(cz, nz);
       }
-      if (nchunk > 1 && !ctx->copy_stream) {
+      // the ball kernels put the last axis in gridDim.z (<= 65535 of 4..64
+      // planes each): longer slabs are labelled in several launches
+      cz = std::min<int64_t>(cz, kMaxZPlanes);
+      if (pipelined && !ctx->copy_stream) {
         ck(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
         for (auto& e : ctx->chunk_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
       }
@@ -684,7 +689,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
         if (ci > 0) launches += launch_chunk_roll(ctr, st);
         ball_and_shell(gc, lb, ds);
         if (sink) sink_chunks.push_back({c0, c1, sink_event(ctx, ci, st)});
-        if (nchunk > 1) {
+        if (pipelined) {
           cudaEvent_t ev = ctx->chunk_ev[ci % kMaxChunks];
           ck(cudaEventRecord(ev, st), "chunk event");
           ck(cudaStreamWaitEvent(ctx->copy_stream, ev, 0), "chunk wait");
@@ -697,7 +702,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
                "D2H distances");
         }
       }
-      if (nchunk > 1) {  // the call's stream waits for the last copy
+      if (pipelined) {  // the call's stream waits for the last copy
         ck(cudaEventRecord(ctx->chunk_ev[ci % kMaxChunks], ctx->copy_stream), "copy event");
         ck(cudaStreamWaitEvent(st, ctx->chunk_ev[ci % kMaxChunks], 0), "copy wait");
         labels_copied = true;

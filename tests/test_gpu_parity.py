@@ -521,3 +521,24 @@ def test_dense_mode_vs_reference(kind, per):
     assert np.array_equal(r.labels.labels, lab_ref), int((r.labels.labels != lab_ref).sum())
     assert np.array_equal(r.distances.values.view(np.uint64), dist_ref.view(np.uint64))
     assert np.array_equal(r.histogram, np.bincount(lab_ref, minlength=ns).astype(np.uint64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,counts,ns", [(1, [600000], 3000), (2, [4, 300000], 2000)])
+def test_long_last_axis_vs_reference(d, counts, ns):
+    """Last axes longer than one launch's grid (262,080 planes) are labelled in
+    several z-chunks; bit-exact against the reference library."""
+    import oracle
+    import paper_2201_13234_b200 as vx
+
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    L = np.full(d, 1.3)
+    pos, _ = oracle.generate_uniform_sites(d, L, ns, 0, 1.0, 17)
+    p = oracle.Problem(0, counts, L, True, pos, None, 0.0)
+    lab_ref, dist_ref, _, _ = oracle.ref_tessellate(p)
+    sites, grid = to_vx(p)
+    r = vx.tessellate_fast(sites, grid, distances=True, histogram=True)
+    assert np.array_equal(r.labels.labels, lab_ref)
+    assert np.array_equal(r.distances.values.view(np.uint64), dist_ref.view(np.uint64))
+    assert int(r.histogram.sum()) == int(np.prod(counts))
