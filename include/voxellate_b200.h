@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define VX_ABI_VERSION 1
+#define VX_ABI_VERSION 2
 #define VX_MAX_DIM 16 /* kMaxDim, geometry.hpp:16 */
 
 enum vx_kind { VX_VORONOI = 0, VX_JOHNSON_MEHL = 1, VX_LAGUERRE = 2 };
@@ -77,6 +77,10 @@ typedef struct vx_options {
   int64_t slab_begin;     /* last-axis slab [slab_begin, slab_end) to label;      */
   int64_t slab_end;       /* 0,0 = whole grid.  Outputs then hold only the slab.  */
   double ball_scale;      /* gather radius = ball_scale * r0 (default 0 -> 1.0) */
+  int32_t n_gpus;         /* > 1: split the slab over devices device..device+n_gpus-1 (wrapping
+                             onto the devices present), one host thread each; host
+                             buffers only (one process per GPU for device-resident data) */
+  int32_t reserved;
 } vx_options;
 
 /* EvalCounters / param of TessResult (tessellate.hpp:31-43) for this engine. */

@@ -117,6 +117,7 @@ struct TessResult {
 struct FastOptions {
   std::optional<double> override_param;
   bool prune = true;
+  int n_gpus = 1;  // extension: split the call over this many devices
 };
 struct PruneResult {
   SiteSet sites;
@@ -160,6 +161,7 @@ inline TessResult run(const SiteSet& s, const VoxelGrid& g, const FastOptions* o
   vx_options_init(&O);
   if (o) {
     O.prune = o->prune ? 1 : 0;
+    O.n_gpus = o->n_gpus;
     if (o->override_param) {
       O.has_override = 1;
       O.override_param = *o->override_param;

@@ -49,6 +49,8 @@ class vx_options(C.Structure):
         ("slab_begin", C.c_int64),
         ("slab_end", C.c_int64),
         ("ball_scale", C.c_double),
+        ("n_gpus", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 

@@ -22,6 +22,7 @@
 #include <mutex>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "voxellate_b200.h"
@@ -776,6 +777,108 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
   return VX_OK;
 }
 
+// Contexts of the multi-GPU host-buffer path, one per device, kept for the
+// process (single-device calls use per-thread contexts).
+vx_context* pool_context(int dev, int* rc) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<vx_context>> pool;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = pool.find(dev);
+  if (it != pool.end()) return it->second.get();
+  vx_context* c = nullptr;
+  *rc = create_context(dev, &c);
+  if (*rc) return nullptr;
+  pool[dev].reset(c);
+  return c;
+}
+
+// options->n_gpus > 1 (host buffers): rank r of G labels the last-axis slab of
+// the reference's per-thread formula (tessellate.cpp:120-121) on device
+// (device + r) mod (devices present), from its own host thread, straight into
+// its part of the caller's buffers; the partial histograms are summed here.
+// Results are bit-identical to a one-device call.
+int run_multi(const vx_problem* P, const vx_options& O, int32_t* labels_out, vx_stats* stats, bool brute) {
+  int rc = check_problem(P);
+  if (rc) return rc;
+  if (O.device_pointers || O.asynchronous)
+    return fail(VX_EUNSUPPORTED,
+                "n_gpus > 1 needs host buffers (device-resident data: one process per GPU with slabs)");
+  if (!labels_out) return fail(VX_EINVAL, "labels_out must not be NULL");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(VX_ECUDA, "no CUDA device available");
+  }
+  int dev0 = O.device;
+  if (dev0 < 0 && cudaGetDevice(&dev0) != cudaSuccess) dev0 = 0;
+  const int d = P->dim;
+  const int64_t n_last = P->counts[d - 1];
+  int64_t zb = O.slab_begin, ze = O.slab_end;
+  if (zb == 0 && ze == 0) ze = n_last;
+  if (!(zb >= 0 && zb < ze && ze <= n_last))
+    return fail(VX_EINVAL, "slab must satisfy 0 <= slab_begin < slab_end <= counts[dim-1]");
+  int64_t plane = 1;
+  for (int i = 0; i < d - 1; ++i) plane *= P->counts[i];
+  const int G = O.n_gpus;
+  const int64_t ns = P->n_sites;
+  std::vector<std::vector<uint64_t>> hist(O.histogram_out ? G : 0);
+  std::vector<vx_stats> st(G);
+  std::vector<int> rcs(G, VX_OK);
+  std::vector<std::string> errs(G);
+  std::vector<std::thread> th;
+  for (int r = 0; r < G; ++r) {
+    int64_t a = 0, b = 0;
+    vx_slab_bounds(ze - zb, r, G, &a, &b);
+    if (b <= a) continue;
+    a += zb;
+    b += zb;
+    th.emplace_back([&, r, a, b] {
+      const int dev = (dev0 + r) % ndev;
+      int rr = VX_OK;
+      vx_context* ctx = pool_context(dev, &rr);
+      if (!ctx) {
+        rcs[r] = rr;
+        errs[r] = vx_last_error();
+        return;
+      }
+      vx_options o = O;
+      o.n_gpus = 1;
+      o.device = dev;
+      o.slab_begin = a;
+      o.slab_end = b;
+      o.distances_out = O.distances_out ? O.distances_out + (a - zb) * plane : nullptr;
+      if (O.histogram_out) {
+        hist[r].assign((size_t)ns, 0);
+        o.histogram_out = hist[r].data();
+      }
+      std::memset(&st[r], 0, sizeof(vx_stats));
+      rcs[r] = run(ctx, P, &o, labels_out + (a - zb) * plane, &st[r], brute);
+      if (rcs[r]) errs[r] = vx_last_error();
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int r = 0; r < G; ++r)
+    if (rcs[r]) return fail(rcs[r], errs[r]);
+  if (O.histogram_out) {
+    std::memset(O.histogram_out, 0, sizeof(uint64_t) * ns);
+    for (const auto& h : hist)
+      for (size_t i = 0; i < h.size(); ++i) O.histogram_out[i] += h[i];
+  }
+  if (stats) {
+    *stats = st[0];
+    for (int r = 1; r < G; ++r) {
+      stats->n_voxels += st[r].n_voxels;
+      stats->n_unresolved += st[r].n_unresolved;
+      stats->ball_evals += st[r].ball_evals;
+      stats->shell_evals += st[r].shell_evals;
+      stats->kernel_launches += st[r].kernel_launches;
+      stats->overflow_bricks += st[r].overflow_bricks;
+      for (int k = 0; k < 8; ++k) stats->stage_ms[k] = std::max(stats->stage_ms[k], st[r].stage_ms[k]);
+    }
+  }
+  return VX_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -841,11 +944,13 @@ int64_t vx_context_workspace_bytes(const vx_context* ctx) {
 
 int vx_tessellate(vx_context* ctx, const vx_problem* problem, const vx_options* options,
                   int32_t* labels_out, vx_stats* stats_out) {
+  if (options && options->n_gpus > 1) return run_multi(problem, *options, labels_out, stats_out, false);
   return run(ctx, problem, options, labels_out, stats_out, false);
 }
 
 int vx_tessellate_brute(vx_context* ctx, const vx_problem* problem, const vx_options* options,
                         int32_t* labels_out, vx_stats* stats_out) {
+  if (options && options->n_gpus > 1) return run_multi(problem, *options, labels_out, stats_out, true);
   return run(ctx, problem, options, labels_out, stats_out, true);
 }
 

@@ -237,7 +237,7 @@ def _problem(sites: SiteSet, grid: VoxelGrid) -> vx_problem:
 
 def _run(engine: str, sites: SiteSet, grid: VoxelGrid, options: Optional[FastOptions],
          distances: bool, histogram: bool, slab, device, ball_scale, context=None, out=None,
-         profile=False) -> TessResult:
+         profile=False, n_gpus=None) -> TessResult:
     P = _problem(sites, grid)
     O = vx_options()
     lib().vx_options_init(C.byref(O))
@@ -250,6 +250,8 @@ def _run(engine: str, sites: SiteSet, grid: VoxelGrid, options: Optional[FastOpt
         O.device = int(device)
     if ball_scale is not None:
         O.ball_scale = float(ball_scale)
+    if n_gpus is not None:
+        O.n_gpus = int(n_gpus)
     zb, ze = (0, grid.counts[-1]) if slab is None else (int(slab[0]), int(slab[1]))
     O.slab_begin, O.slab_end = zb, ze
     plane = grid.voxel_count() // grid.counts[-1]
@@ -277,12 +279,13 @@ def _run(engine: str, sites: SiteSet, grid: VoxelGrid, options: Optional[FastOpt
 
 def tessellate_fast(sites: SiteSet, grid: VoxelGrid, options: Optional[FastOptions] = None, *,
                     distances: bool = True, histogram: bool = False, slab=None, device=None,
-                    ball_scale=None, context=None, out=None, profile=False) -> TessResult:
+                    ball_scale=None, context=None, out=None, profile=False, n_gpus=None) -> TessResult:
     """Two-step engine on the GPU (tessellate.cpp:195-282).  ``slab=(z0, z1)``
     labels only last-axis planes [z0, z1) (the multi-GPU decomposition);
-    ``out`` receives the labels (e.g. a pinned host buffer)."""
+    ``out`` receives the labels (e.g. a pinned host buffer); ``n_gpus`` splits
+    the call over that many devices from one process."""
     return _run("fast", sites, grid, options or FastOptions(), distances, histogram, slab, device,
-                ball_scale, context, out, profile)
+                ball_scale, context, out, profile, n_gpus)
 
 
 def tessellate_brute(sites: SiteSet, grid: VoxelGrid, *, distances: bool = True,

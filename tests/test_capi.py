@@ -51,7 +51,7 @@ def test_version_and_options_defaults():
     import paper_2201_13234_b200 as vx
     from paper_2201_13234_b200._lib import vx_options
 
-    assert vx.lib().vx_abi_version() == 1
+    assert vx.lib().vx_abi_version() == 2
     o = vx_options()
     vx.lib().vx_options_init(C.byref(o))
     assert o.prune == 1 and o.device == -1 and o.ball_scale == 1.0 and o.device_pointers == 0

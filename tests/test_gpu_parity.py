@@ -542,3 +542,27 @@ def test_long_last_axis_vs_reference(d, counts, ns):
     assert np.array_equal(r.labels.labels, lab_ref)
     assert np.array_equal(r.distances.values.view(np.uint64), dist_ref.view(np.uint64))
     assert int(r.histogram.sum()) == int(np.prod(counts))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_gpus", [2, 3])
+def test_n_gpus_single_call_identical(n_gpus):
+    """options.n_gpus splits one call over devices (wrapping onto the devices
+    present, one host thread each); labels, values, histogram and counts equal
+    the one-device call."""
+    import oracle
+    import paper_2201_13234_b200 as vx
+
+    for kind, per in [(0, True), (1, False), (2, True)]:
+        rng = np.random.default_rng(40 + kind)
+        L = rng.uniform(0.6, 1.4, 3)
+        pos, t = oracle.generate_uniform_sites(3, L, 900, kind, 1.0, 71 + kind)
+        p = oracle.Problem(kind, [64, 48, 101], L, per, pos, t, 0.0 if kind == 0 else 0.8)
+        sites, grid = to_vx(p)
+        a = vx.tessellate_fast(sites, grid, vx.FastOptions(prune=True), distances=True, histogram=True)
+        b = vx.tessellate_fast(sites, grid, vx.FastOptions(prune=True), distances=True, histogram=True,
+                               n_gpus=n_gpus)
+        assert np.array_equal(a.labels.labels, b.labels.labels)
+        assert np.array_equal(a.distances.values.view(np.uint64), b.distances.values.view(np.uint64))
+        assert np.array_equal(a.histogram, b.histogram)
+        assert b.stats["n_voxels"] == p.n_voxels
