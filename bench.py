@@ -365,7 +365,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-planes", type=int, default=320)  # ~10 s of reference CPU work at cfg5
-    ap.add_argument("--ref-planes", type=int, default=32)
+    # 320 planes: the sampled rate matches a full reference run on the box (fixed per-call costs amortised)
+    ap.add_argument("--ref-planes", type=int, default=320)
     # functional dry run of the N > 1 path on a one-GPU box (not a measurement):
     # gloo collectives, every rank on cuda:0
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"], help=argparse.SUPPRESS)
