@@ -149,3 +149,22 @@ def test_prune_rejects_voronoi():
     box, s = _sites(kind=0)
     with pytest.raises(ValueError, match="timed tessellations only"):
         vx.prune_ineffective_sites(s, box)
+
+
+@pytest.mark.parametrize("where", [0, 123456, 299999])
+def test_large_site_set_validation_threads(where):
+    """The host position check is split over threads for large site sets; a
+    bad coordinate anywhere gives the reference's message (sites.cpp:54-57)
+    before any device work."""
+    import numpy as np
+
+    import paper_2201_13234_b200 as vx
+
+    n = 300000
+    pos = np.random.default_rng(3).uniform(0.01, 0.99, 3 * n)
+    pos[3 * where + 1] = 1.0  # on the boundary: not strictly inside
+    box = vx.Domain([1.0, 1.0, 1.0], vx.Boundary.Periodic)
+    grid = vx.VoxelGrid([8, 8, 8], box)
+    sites = vx.SiteSet(vx.Kind.Voronoi, 3, pos, None, 0.0)
+    with pytest.raises(ValueError, match="site positions must lie strictly inside the domain"):
+        vx.tessellate_fast(sites, grid)
