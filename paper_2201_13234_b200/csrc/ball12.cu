@@ -237,6 +237,11 @@ __global__ void __launch_bounds__(kB2Threads, 4)
   };
   const double R = prm->gather_r;
   const double cutoff = prm->cutoff;
+  // the cutoff rounded up to f32: a site whose lower bound exceeds it over a
+  // brick has prox > cutoff at every voxel there, so it can neither win a
+  // resolved voxel nor matter at an unresolved one -- every cull level is
+  // clamped to it (a partly uncovered brick keeps only reachable sites)
+  const float tcf = __double2float_ru(cutoff + 1e-9 * fabs(cutoff));
   float halfLf[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) halfLf[a] = (float)g.halfL[a];
@@ -424,6 +429,10 @@ __global__ void __launch_bounds__(kB2Threads, 4)
     atomicAdd(&eval_slots[66], 1ull);
     atomicMax(&eval_slots[71], (unsigned long long)T);
   }
+  // no site reaches the super-brick within the cutoff (T == 0): every voxel
+  // is outside every ball (the reference's step-2 set) -- empty brick lists,
+  // not an overflow
+  const bool lists_ok = rows_ok && T <= kTcap;
   cta_ok = cta_ok && T > 0 && T <= kTcap;
 
   // ---------------- W + S: per-warp column of nbb bricks ----------------
@@ -497,7 +506,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       float t = myub[b];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) t = fminf(t, __shfl_xor_sync(0xffffffffu, t, o));
-      tau[b] = t;
+      tau[b] = fminf(t, tcf);
     }
     for (int f = lane; f < T; f += 32) {
       const float4 s = S.rel[f];
@@ -532,7 +541,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
   if (bext[0] <= 0 || bext[1] <= 0 || bext[2] <= 0) continue;
 
   int nW = 0;
-  bool brick_ok = cta_ok;
+  bool brick_ok = lists_ok;
   if (brick_ok) {
     for (int f0 = 0; f0 < T; f0 += 32) {
       const int f = f0 + lane < T ? S.ord[f0 + lane] : 0;
@@ -578,11 +587,11 @@ __global__ void __launch_bounds__(kB2Threads, 4)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) km = min(km, __shfl_xor_sync(0xffffffffu, km, o));
       const int r0 = (int)(km & 255u);
-      const int fr = ws.W[r0];
+      const int fr = nW > 0 ? ws.W[r0] : 0;  // empty list (n2 = 0): any in-bounds slot
       const unsigned fl0 = S.flag[fr];
       SiteF z;  // every lane derives the reference's bounds itself
       fbounds<KIND, PER>(S.rel[fr], fl0, Bs, halfLf, invG, z);
-      const float tau = z.ubp;  // >= the minimum upper bound: a valid cull level
+      const float tau = fminf(z.ubp, tcf);  // >= the minimum upper bound: a valid cull level
       for (int c0 = 0; c0 < nW; c0 += 32) {
         const int k = c0 + lane;
         bool keep = false;
@@ -651,7 +660,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       z.t = __shfl_sync(0xffffffffu, rhi ? sb.t : sa.t, rl);
       z.lb = __shfl_sync(0xffffffffu, rhi ? sb.lb : sa.lb, rl);
       z.ub = __shfl_sync(0xffffffffu, rhi ? sb.ub : sa.ub, rl);
-      const float tau = __shfl_sync(0xffffffffu, rhi ? sb.ubp : sa.ubp, rl);
+      const float tau = fminf(__shfl_sync(0xffffffffu, rhi ? sb.ubp : sa.ubp, rl), tcf);
       const unsigned fl0 = __shfl_sync(0xffffffffu, rhi ? flb : fla, rl);
       const bool ka = va && (lane == r0 || (sa.lbp <= tau &&
                                             bisector_keep<KIND, PER>(sa, fla, z, fl0, Bs, halfLf, invG, e_d)));
@@ -687,7 +696,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sbi;
     }
   }
-  if (lane == 0 && !(cta_ok && brick_ok)) atomicAdd(&ctr->overflow_bricks, 1ull);
+  if (lane == 0 && !brick_ok) atomicAdd(&ctr->overflow_bricks, 1ull);
   }  // bb
 }
 

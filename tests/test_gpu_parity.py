@@ -566,3 +566,81 @@ def test_n_gpus_single_call_identical(n_gpus):
         assert np.array_equal(a.distances.values.view(np.uint64), b.distances.values.view(np.uint64))
         assert np.array_equal(a.histogram, b.histogram)
         assert b.stats["n_voxels"] == p.n_voxels
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,kind,periodic", [(2, 1, True), (3, 0, True), (3, 1, False), (3, 2, True), (3, 0, False)])
+def test_refinement_preserves_labels_at_shared_centres(d, kind, periodic):
+    """test_tessellate.cpp:365-387: spacings 3/4 and 1/4 give exactly equal
+    centres at coarse voxel i and fine voxel 3i+1, so the fast engine on the
+    fine grid must reproduce the coarse grid's labels and f64 values there."""
+    import oracle
+
+    L = [3.0] * d if d == 2 else [12.0, 9.0, 6.0]
+    coarse = [int(round(x / 0.75)) for x in L]
+    fine = [3 * c for c in coarse]
+    ns = 20 if d == 2 else 300
+    horizon = 0.5 * float(np.prod(L)) ** (1.0 / d) / ns ** (1.0 / d)
+    pos, t = oracle.generate_uniform_sites(d, np.array(L), ns, kind, horizon, 606 + kind)
+    G = [0.0, 1.3, 0.8][kind]
+    pc = oracle.Problem(kind, coarse, L, periodic, pos, t, G)
+    pf = oracle.Problem(kind, fine, L, periodic, pos, t, G)
+    c = run_brute(pc)
+    f = run_fast(pf)
+    cl = c.labels.labels.reshape(coarse[::-1])
+    fl = f.labels.labels.reshape(fine[::-1])
+    cv = c.distances.values.reshape(coarse[::-1])
+    fv = f.distances.values.reshape(fine[::-1])
+    sl = tuple(slice(1, None, 3) for _ in range(d))
+    assert np.array_equal(fl[sl], cl)
+    assert np.array_equal(bits(fv[sl]), bits(cv))
+
+
+def coverage_case(i):
+    """Random near-isotropic instance for the ball-coverage test (shared with
+    scripts/cov_probe.py)."""
+    import oracle
+
+    rng = np.random.default_rng(2480 + i)
+    kind = i % 3
+    periodic = i % 2 == 0
+    d = 2 if i == 7 else 3
+    counts = [int(x) for x in rng.integers(48, 97, d)]
+    L = np.array(counts) * rng.uniform(0.01, 0.02) * rng.uniform(0.9, 1.1, d)
+    spacing = float(rng.uniform(9.0, 16.0))
+    ns = max(2, int(np.prod(counts) / spacing ** d))
+    horizon = float(0.5 * np.prod(L) ** (1.0 / d) / ns ** (1.0 / d))
+    pos, t = oracle.generate_uniform_sites(d, L, ns, kind, horizon, 77 + i)
+    return oracle.Problem(kind, counts, L, periodic, pos, t, [0.0, 1.1, 0.9][kind])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("i", range(8))
+def test_ball_phase_covers_exactly_the_union_of_balls(i):
+    """test_tessellate.cpp:248-269: the voxels the ball phase leaves to the
+    shell search are exactly those outside every investigation ball.  The
+    reference's step 2 evaluates every kept site at each such voxel, so its
+    count is step2_evals / n_sites; ours is the unresolved-voxel counter.
+
+    Both engines run with the reference's own parameter (our t0 search for the
+    timed kinds picks its own t0 -- labels never depend on it), and the
+    instances keep voxels near-isotropic so no sub-brick takes the overflow
+    route (whose voxels are labelled by the sub-brick shell instead)."""
+    import oracle
+
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    p = coverage_case(i)
+    ns = p.n_sites
+    _, _, param, _ = oracle.ref_tessellate(p, prune=False, distances=False)
+    tmin = 0.0 if p.kind == 0 else float(np.min(p.times))
+    for scale in (1.0, 0.5):  # the reference's ball, then a smaller one
+        override = param * scale if p.kind == 0 else tmin + scale * (param - tmin)
+        lab_ref, _, param_ref, (_, ev2) = oracle.ref_tessellate(p, prune=False, override=override,
+                                                                 distances=False)
+        r = run_fast(p, prune=False, override=override, distances=False)
+        assert r.param == param_ref == override
+        assert np.array_equal(r.labels.labels, lab_ref)
+        assert r.stats["overflow_bricks"] == 0
+        assert ev2 % ns == 0
+        assert r.stats["n_unresolved"] == ev2 // ns, (r.stats["n_unresolved"], ev2 // ns)
