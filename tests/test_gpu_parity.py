@@ -7,8 +7,11 @@ test_tessellate.cpp:55-86 (hand-checked), :178-216 and acceptance.cpp:49-113
 (fast == brute bitwise over random instances), :218-246 (extreme r0), :292-310
 (equal birth times -> Voronoi), :312-341 (validate_partition), :343-363
 (worker-count independence -> slab/GPU-count independence), test_sites.cpp
-:125-143,173-194 (coincident sites, prune preserves partitions), plus the five
-BASELINE configs against the reference's label fingerprints (App. B).
+:125-143,173-194 (coincident sites, prune preserves partitions),
+test_tessellate.cpp:248-269 (step 1 covers exactly the union of the balls),
+:365-387 (grid refinement keeps labels at shared centres), lattice instances
+full of exact ties, plus the five BASELINE configs against the reference's
+label fingerprints (App. B).
 """
 import ctypes as C
 import os
@@ -644,3 +647,76 @@ def test_ball_phase_covers_exactly_the_union_of_balls(i):
         assert r.stats["overflow_bricks"] == 0
         assert ev2 % ns == 0
         assert r.stats["n_unresolved"] == ev2 // ns, (r.stats["n_unresolved"], ev2 // ns)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,periodic,n,step", [(0, True, 64, 8), (0, False, 64, 8), (1, True, 48, 4),
+                                                   (2, True, 64, 8), (2, False, 48, 6), (0, True, 40, 5)])
+def test_lattice_ties_lowest_index_wins(oracle_mod, kind, periodic, n, step):
+    """Exact ties everywhere: sites on voxel centres of a regular lattice
+    (`step` voxels apart, spacing 1/64 so every coordinate is dyadic), so each
+    voxel half-way between lattice sites -- across the periodic boundary too --
+    is exactly equidistant from 2, 4 or 8 of them.  The site order is a random
+    permutation, so the lowest-index rule (strict `<` over ascending index,
+    tessellate.cpp:65; test_sites.cpp:125-143) decides a large share of the
+    image.  Timed kinds draw each birth time from two dyadic values: equal
+    times tie exactly, unequal ones do not."""
+    rng = np.random.default_rng(n * 31 + step + kind)
+    Ln = n / 64.0
+    sp = Ln / n
+    k = np.arange(0, n, step)
+    g = np.stack(np.meshgrid(k, k, k, indexing="ij"), -1).reshape(-1, 3)
+    g = g[rng.permutation(len(g))]
+    pos = ((g + 0.5) * sp).reshape(-1)
+    t = rng.choice([0.0, 0.0078125], len(g)) if kind else None
+    p = oracle_mod.Problem(kind, [n, n, n], [Ln] * 3, periodic, pos, t, [0.0, 1.0, 0.5][kind])
+    lab_all, dist_all = oracle_mod.brute(p)
+    assert len(np.unique(lab_all)) > 1
+    for prune in (True, False):
+        lab, dist = lab_all, dist_all
+        if prune and kind != 0:  # the reference labels the prune survivors
+            dropped = oracle_mod.prune(p)
+            if dropped.any():
+                keep = np.nonzero(dropped == 0)[0]
+                q = oracle_mod.Problem(kind, p.counts, p.lengths, periodic,
+                                       p.positions.reshape(-1, 3)[keep].reshape(-1), p.times[keep], p.growth)
+                l2, dist = oracle_mod.brute(q)
+                lab = keep[l2].astype(np.uint32)
+        r = run_fast(p, prune=prune)
+        assert np.array_equal(r.labels.labels, lab), int((r.labels.labels != lab).sum())
+        assert np.array_equal(bits(r.distances.values), bits(dist))
+    rb = run_brute(p)
+    assert np.array_equal(rb.labels.labels, lab_all)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,periodic", [(0, True), (0, False), (1, True), (2, False), (2, True)])
+def test_sites_hugging_the_domain_faces(oracle_mod, kind, periodic):
+    """Sites at the extremes the reference accepts (sites.cpp:55: 0 < x < L):
+    coordinates one ulp above 0 and one ulp below L, on faces, edges and
+    corners, mixed with interior sites -- the binning, the periodic wrap of
+    the cull's f32 frame and the exact fold all meet their edge cases here."""
+    rng = np.random.default_rng(9100 + 10 * kind + periodic)
+    L = np.array([1.0, 0.8125, 1.375])
+    counts = [48, 40, 56]
+    lo, hi = np.nextafter(0.0, 1.0), np.nextafter(L, 0.0)
+    interior = rng.uniform(0.05, 0.95, (120, 3)) * L
+    edge = []
+    for _ in range(80):
+        q = rng.uniform(0.0, 1.0, 3) * L
+        for a in range(3):
+            r = rng.integers(3)
+            if r == 0:
+                q[a] = lo if rng.integers(2) else np.nextafter(lo, 1.0)
+            elif r == 1:
+                q[a] = hi[a] if rng.integers(2) else np.nextafter(hi[a], 0.0)
+        edge.append(q)
+    pts = np.concatenate([interior, np.array(edge)])
+    pts = pts[rng.permutation(len(pts))]
+    assert (pts > 0).all() and (pts < L).all()
+    t = rng.uniform(0.0, 0.05, len(pts)) if kind else None
+    p = oracle_mod.Problem(kind, counts, L, periodic, pts.reshape(-1), t, [0.0, 1.2, 0.7][kind])
+    lab, dist = oracle_mod.brute(p)
+    r = run_fast(p, prune=False)
+    assert np.array_equal(r.labels.labels, lab), int((r.labels.labels != lab).sum())
+    assert np.array_equal(bits(r.distances.values), bits(dist))
