@@ -203,6 +203,11 @@ int vx_image_sidecar_text(const char* type, int dim, const int64_t* counts, cons
 /* sustained f64 DADD and f32 FADD issue rates (adds/s) of `device`; the
  * roofline denominator for the per-voxel evaluation kernels */
 int vx_probe_pipe_rates(int device, double* dadd_per_s, double* fadd_per_s);
+/* Checks the eval kernel's call-free correctly rounded sqrt / division against
+ * __dsqrt_rn / __ddiv_rn on n seeded random inputs (division by growth);
+ * writes the number of bitwise mismatches of each. */
+int vx_probe_exact_arith(int device, uint64_t n, uint64_t seed, double growth,
+                         uint64_t* sqrt_mismatches, uint64_t* div_mismatches);
 
 #ifdef __cplusplus
 }

@@ -73,12 +73,14 @@ struct FBox {
 struct __align__(16) WarpSmem {
   int W[kWcapD];       // brick list (gather slots), ascending site index
   int L[kLcapD];       // dense mode: a sub-brick's survivors (binned positions)
+  unsigned evals;      // exact evaluations the eval kernel will do for this warp's sub-bricks
 };
 
 // eval12: per warp (one sub-brick); LC = list capacity
 template <int LC>
 struct __align__(16) EvalSmemT {
   double T[kFcap][20]; // exact w^2 of one pass of kFcap candidates: [0,8) x, [8,16) y, [16,20) z
+  double C[24];        // the sub-brick's voxel centres: [0,8) x, [8,16) y, [16,24) z
   double Ft[LC];
   int P[LC];           // binned positions
   int Fidx[LC];
@@ -437,6 +439,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
 
   // ---------------- W + S: per-warp column of nbb bricks ----------------
   WarpSmem& ws = S.w[wid];
+  if (lane == 0) ws.evals = 0;  // lane 0 alone updates it
   const int bxo = (wid & 1) * 8, byo = ((wid >> 1) & 1) * 8;
 
   auto box_of = [&](int x0, int y0, int z0, int nx, int ny, int nz) {
@@ -627,6 +630,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       if (lane == 0) {
         info[sbi] = ok ? make_int2(base, n2) : make_int2(0, -1);
         if (!ok) ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sbi;
+        if (ok) ws.evals += (unsigned)(n2 * sext[0] * sext[1] * sext[2]);
       }
     } else if (brick_ok) {
       const FBox Bs = box_of(bxo, sy, sz, sext[0], sext[1], sext[2]);
@@ -689,6 +693,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       if (lane == 0) {
         info[sbi] = ok ? make_int2(base, n2) : make_int2(0, -1);
         if (!ok) ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sbi;
+        if (ok && n2 <= kFcap) ws.evals += (unsigned)(n2 * sext[0] * sext[1] * sext[2]);
       }
     } else if (lane == 0) {
       const long long sbi = sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz);
@@ -698,6 +703,44 @@ __global__ void __launch_bounds__(kB2Threads, 4)
   }
   if (lane == 0 && !brick_ok) atomicAdd(&ctr->overflow_bricks, 1ull);
   }  // bb
+  // the ball-phase evaluation counter (EvalCounters::step1_evals), one atomic per warp
+  if (lane == 0 && ws.evals)
+    atomicAdd(&eval_slots[(blockIdx.x + 8 * blockIdx.y + wid) & 63], (unsigned long long)ws.evals);
+}
+
+// exact per-axis tables (the reference arithmetic): one lane per (site, axis)
+// computes w^2 at the sub-brick's 8 (z: 4) voxel centres; u = site - centre
+// (geometry.hpp:58-60) is wrapped only when |u| >= 0.49 L -- below that
+// floor(u/L + 0.5) == 0 and the reference's wrap returns u itself
+template <bool PER, class ES>
+__device__ __forceinline__ void exact_tables(ES& ws, const Bins& bins, const Geo& g, int lane, int c0, int m) {
+  for (int e = lane; e < 3 * m; e += 32) {
+    const int a = e >= 2 * m ? 2 : (e >= m ? 1 : 0);
+    const int j = e - a * m;
+    const int p = ws.P[c0 + j];
+    const double* sa = a == 0 ? bins.x : (a == 1 ? bins.y : bins.z);
+    const double sv = sa[p];
+    const double* cr = &ws.C[a * 8];
+    double u[8];
+    bool far = false;
+    const double La = PER ? (a == 0 ? g.L[0] : (a == 1 ? g.L[1] : g.L[2])) : 0.0;
+    const double lim = 0.49 * La;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      u[r] = __dsub_rn(sv, cr[r]);
+      if (PER) far |= !(fabs(u[r]) < lim);
+    }
+    if (PER && far) {  // rare: a site about half a period away
+      const double iLa = a == 0 ? g.invL[0] : (a == 1 ? g.invL[1] : g.invL[2]);
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (!(fabs(u[r]) < lim)) u[r] = wrap_delta(u[r], La, iLa);
+    }
+    double* trow = &ws.T[j][a * 8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (r < 4 || a != 2) trow[r] = __dmul_rn(u[r], u[r]);
+  }
 }
 
 constexpr int kEvalWarps = 2;  // sub-bricks along y per CTA
@@ -705,7 +748,7 @@ constexpr int kEvalWarps = 2;  // sub-bricks along y per CTA
 // One warp per 8x8x4 sub-brick (the tail of v11's sub-brick loop: exact
 // tables, evaluation, stores, histogram, unresolved compaction).  The site
 // index load is issued before the tables and consumed at the store.
-template <int KIND, bool PER, bool DENSE>
+template <int KIND, bool PER, bool DENSE, bool FA>
 __global__ void __launch_bounds__(kEvalWarps * 32, 16)
     eval12_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, const int2* __restrict__ info,
                   const int* __restrict__ slots16, const int* __restrict__ list, int* __restrict__ labels,
@@ -716,9 +759,8 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 16)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   using ES = EvalSmemT<DENSE ? kLcapD : kFcap>;
   ES& ws = reinterpret_cast<ES*>(smem_raw)[wid];
-  const unsigned nsbx = (unsigned)((g.n[0] + 7) / 8), nsby = (unsigned)((g.n[1] + 7) / 8);
+  const unsigned nsbx = g.nsbx, nsby = g.nsby;
   const double cutoff = prm->cutoff;
-  const long long slab_base = g.z_begin * g.n[0] * g.n[1];
   const int qx = (lane & 1) * 4, vy = (lane >> 1) & 3, vz = lane >> 3;
   // grid (nsbx, ceil(nsby / 8), nsbz): no index division
   const unsigned sbx = blockIdx.x, sby = blockIdx.y * kEvalWarps + wid, sbz = blockIdx.z;
@@ -751,6 +793,11 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 16)
         if (KIND != kVoronoi) ws.Ft[lane] = bins.t[pl];
       }
     }
+    if (lane < 24 && n2 > 0) {  // the sub-brick's voxel centres, once (geometry.hpp:58-60)
+      const int a = lane >> 3;
+      const long long k0 = a == 0 ? x0 : (a == 1 ? y0 : z0);
+      ws.C[lane] = center(k0 + (lane & 7), a == 0 ? g.sp[0] : (a == 1 ? g.sp[1] : g.sp[2]));
+    }
     __syncwarp();
     auto store_tail = [&](double (&best)[8], int (&bj)[8]) {
     // resolve + store + compaction of unresolved voxels
@@ -759,16 +806,19 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 16)
     }
     __syncwarp();
 
-    const long long kz = z0 + vz;
-    const long long lin0 = x0 + qx + g.n[0] * (y0 + vy + g.n[1] * kz);
+    // voxel offset inside the slab (the unresolved list holds absolute indices)
+    const long long lrel = (long long)(sbz * 4 + vz) * g.plane + (long long)(y0 + vy) * g.n[0] + x0 + qx;
     const long long rstep = 4 * g.n[0];  // row vy -> vy + 4
+    // bit k: voxel k of this lane lies inside the grid
+    const int xr = sext[0] - qx;
+    const unsigned xm = xr >= 4 ? 0xFu : (xr > 0 ? (1u << xr) - 1u : 0u);
+    const unsigned vmask = vz < sext[2] ? ((vy < sext[1] ? xm : 0u) | (vy + 4 < sext[1] ? xm << 4 : 0u)) : 0u;
     int lab[8];
     unsigned umask = 0;  // bit k: voxel k valid but unresolved
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       lab[k] = -1;
-      const bool valid = (k < 4 ? vy : vy + 4) < sext[1] && vz < sext[2] && qx + (k & 3) < sext[0];
-      if (valid) {
+      if ((vmask >> k) & 1u) {
         if (best[k] <= cutoff) {  // best = +inf when there is no candidate
           lab[k] = ws.Fidx[bj[k]];
           if (hist) atomicAdd(&ws.cnt[bj[k]], 1);
@@ -779,21 +829,20 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 16)
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const bool rv = (vy + 4 * h) < sext[1] && vz < sext[2];
-      if (!rv) continue;
-      int* out = labels + (lin0 + h * rstep - slab_base);
-      if (qx + 4 <= sext[0] && g.vec_store) {
+      if (!((vmask >> (4 * h)) & 0xFu)) continue;
+      int* out = labels + (lrel + h * rstep);
+      if (xm == 0xFu && g.vec_store) {
         *reinterpret_cast<int4*>(out) = make_int4(lab[4 * h], lab[4 * h + 1], lab[4 * h + 2], lab[4 * h + 3]);
       } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (qx + k < sext[0]) out[k] = lab[4 * h + k];
+          if ((xm >> k) & 1u) out[k] = lab[4 * h + k];
       }
       if (dist) {
-        double* dout = dist + (lin0 + h * rstep - slab_base);
+        double* dout = dist + (lrel + h * rstep);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (qx + k < sext[0] && lab[4 * h + k] >= 0)
+          if (((xm >> k) & 1u) && lab[4 * h + k] >= 0)
             dout[k] = KIND == kVoronoi ? __dsqrt_rn(best[4 * h + k]) : best[4 * h + k];
       }
     }
@@ -814,11 +863,9 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 16)
       for (int i = 0; i < nun; ++i) {
         const int k = __ffs(mm) - 1;
         mm &= mm - 1;
-        if (off + i < unres_cap) unres[off + i] = lin0 + (k < 4 ? 0 : rstep) + (k & 3);
+        if (off + i < unres_cap) unres[off + i] = g.z_begin * g.plane + lrel + (k < 4 ? 0 : rstep) + (k & 3);
       }
     }
-    if (lane == 0 && n2)
-      atomicAdd(&eval_slots[sb & 63], (unsigned long long)n2 * (sext[0] * sext[1] * sext[2]));
     if (hist && n2 > 0) {
       __syncwarp();
       for (int i = lane; i < (DENSE ? n2 : min(n2, 32)); i += 32)
@@ -838,27 +885,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 16)
       // over, so the scan order is still ascending site index
       for (int c0 = 0; c0 < n2; c0 += kFcap) {
         const int m = min(kFcap, n2 - c0);
-    // exact per-axis tables (the reference arithmetic): one lane per (site, axis)
-    for (int e = lane; e < 3 * m; e += 32) {
-      const int a = e >= 2 * m ? 2 : (e >= m ? 1 : 0);
-      const int j = e - a * m;
-      const int p = ws.P[c0 + j];
-      const double sv = a == 0 ? bins.x[p] : (a == 1 ? bins.y[p] : bins.z[p]);
-      const long long k0 = a == 0 ? x0 : (a == 1 ? y0 : z0);
-      const double spa = a == 0 ? g.sp[0] : (a == 1 ? g.sp[1] : g.sp[2]);
-      const double La = a == 0 ? g.L[0] : (a == 1 ? g.L[1] : g.L[2]);
-      const double iLa = a == 0 ? g.invL[0] : (a == 1 ? g.invL[1] : g.invL[2]);
-      const double lim = 0.49 * La;
-      double* trow = &ws.T[j][a * 8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        if (a == 2 && r >= 4) break;
-        const double u = __dsub_rn(sv, center(k0 + r, spa));  // geometry.hpp:58-60
-        // |u| < 0.49 L: floor(u*invL + 0.5) == 0, so the reference's wrap is u itself
-        const double w = (!PER || fabs(u) < lim) ? u : wrap_delta(u, La, iLa);
-        trow[r] = __dmul_rn(w, w);
-      }
-    }
+    exact_tables<PER>(ws, bins, g, lane, c0, m);
     __syncwarp();
     // exact evaluation: lane -> 4 voxels along x in rows vy and vy + 4
     for (int j = 0; j < m; ++j) {
@@ -873,7 +900,8 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 16)
                            __dadd_rn(a1, w23.x), __dadd_rn(a1, w23.y)};
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const double pr = prox_from_dsq<KIND>(d[k], g.growth, g1, tj);
+        const double pr = FA ? prox_from_dsq_nc<KIND>(d[k], g.growth, g1, tj, g.inv_growth_rn)
+                                : prox_from_dsq<KIND>(d[k], g.growth, g1, tj);
         if (pr < best[k]) {
           best[k] = pr;
           bj[k] = c0 + j;
@@ -884,27 +912,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 16)
       }
       store_tail(best, bj);
     } else {
-    // exact per-axis tables (the reference arithmetic): one lane per (site, axis)
-    for (int e = lane; e < 3 * n2; e += 32) {
-      const int a = e >= 2 * n2 ? 2 : (e >= n2 ? 1 : 0);
-      const int j = e - a * n2;
-      const int p = ws.P[j];
-      const double sv = a == 0 ? bins.x[p] : (a == 1 ? bins.y[p] : bins.z[p]);
-      const long long k0 = a == 0 ? x0 : (a == 1 ? y0 : z0);
-      const double spa = a == 0 ? g.sp[0] : (a == 1 ? g.sp[1] : g.sp[2]);
-      const double La = a == 0 ? g.L[0] : (a == 1 ? g.L[1] : g.L[2]);
-      const double iLa = a == 0 ? g.invL[0] : (a == 1 ? g.invL[1] : g.invL[2]);
-      const double lim = 0.49 * La;
-      double* trow = &ws.T[j][a * 8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        if (a == 2 && r >= 4) break;
-        const double u = __dsub_rn(sv, center(k0 + r, spa));  // geometry.hpp:58-60
-        // |u| < 0.49 L: floor(u*invL + 0.5) == 0, so the reference's wrap is u itself
-        const double w = (!PER || fabs(u) < lim) ? u : wrap_delta(u, La, iLa);
-        trow[r] = __dmul_rn(w, w);
-      }
-    }
+    exact_tables<PER>(ws, bins, g, lane, 0, n2);
     __syncwarp();
     // exact evaluation: lane -> 4 voxels along x in rows vy and vy + 4
     double best[8];
@@ -927,7 +935,8 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 16)
                            __dadd_rn(a1, w23.x), __dadd_rn(a1, w23.y)};
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const double pr = prox_from_dsq<KIND>(d[k], g.growth, g1, tj);
+        const double pr = FA ? prox_from_dsq_nc<KIND>(d[k], g.growth, g1, tj, g.inv_growth_rn)
+                                : prox_from_dsq<KIND>(d[k], g.growth, g1, tj);
         if (pr < best[k]) {
           best[k] = pr;
           bj[k] = j;
@@ -1005,7 +1014,10 @@ static void launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* 
   const size_t sh_e = sizeof(v12::EvalSmemT<DENSE ? v12::kLcapD : v12::kFcap>) * v12::kEvalWarps;
   if (!attr) {
     cudaFuncSetAttribute(v12::cull12_kernel<KIND, PER, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_c);
-    cudaFuncSetAttribute(v12::eval12_kernel<KIND, PER, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_e);
+    cudaFuncSetAttribute(v12::eval12_kernel<KIND, PER, DENSE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_e);
+    if (KIND != kVoronoi)
+      cudaFuncSetAttribute(v12::eval12_kernel<KIND, PER, DENSE, KIND != kVoronoi>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_e);
     attr_done.fetch_or(bit);
   }
   const dim3 grid((unsigned)((g.n[0] + v12::kSB - 1) / v12::kSB), (unsigned)((g.n[1] + v12::kSB - 1) / v12::kSB),
@@ -1015,8 +1027,12 @@ static void launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* 
   const long long nsb = ball12_subbricks(g);
   const dim3 eg((unsigned)((g.n[0] + 7) / 8), (unsigned)(((g.n[1] + 7) / 8 + v12::kEvalWarps - 1) / v12::kEvalWarps),
                 (unsigned)((g.z_end - g.z_begin + 3) / 4));
-  v12::eval12_kernel<KIND, PER, DENSE><<<eg, v12::kEvalWarps * 32, sh_e, st>>>(g, bins, prm, info, slots16, list, labels,
-                                                                        dist, hist, unres, cap, ctr, slots, nsb);
+  if (KIND != kVoronoi && g.fast_arith)  // call-free exact sqrt / division (vx_internal.cuh)
+    v12::eval12_kernel<KIND, PER, DENSE, KIND != kVoronoi><<<eg, v12::kEvalWarps * 32, sh_e, st>>>(
+        g, bins, prm, info, slots16, list, labels, dist, hist, unres, cap, ctr, slots, nsb);
+  else
+    v12::eval12_kernel<KIND, PER, DENSE, false><<<eg, v12::kEvalWarps * 32, sh_e, st>>>(
+        g, bins, prm, info, slots16, list, labels, dist, hist, unres, cap, ctr, slots, nsb);
   launch_subshell(g, bins, prm, ovf, &ctr->n_ovf_sb, labels, dist, hist, ctr, st);
 }
 

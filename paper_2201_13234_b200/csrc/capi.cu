@@ -247,6 +247,7 @@ void fill_geo(Geo& g, const vx_problem* P, int64_t zb, int64_t ze, int64_t n_for
   g.has_times = timed(P);
   g.growth = timed(P) ? P->growth : 0.0;
   g.g_is_one = g.growth == 1.0;
+  g.inv_growth_rn = g.growth > 0.0 ? 1.0 / g.growth : 0.0;
   g.lmax = 0.0;
   // true axis a -> embedded axis; the last true axis is always z (see Geo)
   static const int kEmb[4][3] = {{0, 1, 2}, {2, 0, 0}, {0, 2, 0}, {0, 1, 2}};
@@ -295,6 +296,14 @@ void fill_geo(Geo& g, const vx_problem* P, int64_t zb, int64_t ze, int64_t n_for
   }
   g.z_begin = zb;
   g.z_end = ze;
+  g.plane = g.n[0] * g.n[1];
+  {  // range of the call-free exact sqrt / division (vx_internal.cuh)
+    bool ok = g.growth == 0.0 || (g.growth >= 0x1p-64 && g.growth <= 0x1p64);
+    for (int a = 0; a < 3; ++a) ok = ok && g.L[a] >= 0x1p-100 && g.L[a] <= 0x1p100 && g.sp[a] >= 0x1p-120;
+    g.fast_arith = ok && std::getenv("VX_EXACT_CALLS") == nullptr;
+  }
+  g.nsbx = (unsigned)((g.n[0] + 7) / 8);
+  g.nsby = (unsigned)((g.n[1] + 7) / 8);
   g.nbx = (g.n[0] + BX - 1) / BX;
   g.nby = (g.n[1] + BY - 1) / BY;
   g.nbz = (ze - zb + BZ - 1) / BZ;

@@ -3,9 +3,12 @@
 //    the roofline denominator for the ball kernel's evaluations
 //    (MEASURED_PEAKS.json carries only HBM and bf16 figures).
 //  * vx_label_fingerprint: SURVEY.md App. B FNV-style label fingerprint.
+//  * vx_probe_exact_arith: the call-free exact sqrt / division of the eval
+//    kernel (vx_internal.cuh) against __dsqrt_rn / __ddiv_rn, bit for bit.
 #include <cuda_runtime.h>
 
 #include "voxellate_b200.h"
+#include "vx_internal.cuh"
 
 namespace {
 
@@ -56,7 +59,68 @@ double rate(int device) {
   return ops / (best * 1e-3);
 }
 
+__device__ __forceinline__ unsigned long long splitmix(unsigned long long& z) {
+  z += 0x9e3779b97f4a7c15ull;
+  unsigned long long x = z;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+// random doubles with uniform exponent in [e0, e1) and uniform mantissa
+__device__ __forceinline__ double rand_exp(unsigned long long& z, int e0, int e1) {
+  const unsigned long long r = splitmix(z);
+  const int e = e0 + (int)((r >> 52) % (unsigned)(e1 - e0));
+  return __longlong_as_double(((unsigned long long)(e + 1023) << 52) | (r & 0xfffffffffffffull));
+}
+
+__global__ void exact_arith_kernel(unsigned long long n, unsigned long long seed, double G,
+                                   unsigned long long* bad) {
+  const double y = __drcp_rn(G);
+  unsigned long long nb_sqrt = 0, nb_div = 0;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    unsigned long long z = seed ^ (i * 0xd1b54a32d192ed03ull);
+    // squared distances: three squared coordinate differences (uniform mantissas,
+    // exponents over the whole fast range), and plain doubles over the range
+    double x;
+    if (i & 1) {
+      const double u = rand_exp(z, -174, 101), v = rand_exp(z, -174, 101), w = rand_exp(z, -174, 101);
+      x = __dadd_rn(__dadd_rn(__dmul_rn(w, w), __dmul_rn(v, v)), __dmul_rn(u, u));
+    } else {
+      x = rand_exp(z, -348, 210);
+    }
+    if ((i & 1023) == 0) x = 0.0;  // exact zeros (a site on a voxel centre)
+    if (__double_as_longlong(vxb::sqrt_rn_nc(x)) != __double_as_longlong(__dsqrt_rn(x))) ++nb_sqrt;
+    const double a = (i & 2) ? __dsqrt_rn(x) : x;
+    if (__double_as_longlong(vxb::div_rn_nc(a, G, y)) != __double_as_longlong(__ddiv_rn(a, G))) ++nb_div;
+  }
+  if (nb_sqrt) atomicAdd(&bad[0], nb_sqrt);
+  if (nb_div) atomicAdd(&bad[1], nb_div);
+}
+
 }  // namespace
+
+extern "C" int vx_probe_exact_arith(int device, uint64_t n, uint64_t seed, double growth,
+                                    uint64_t* sqrt_mismatches, uint64_t* div_mismatches) {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess) return VX_ECUDA;
+  unsigned long long* bad = nullptr;
+  if (cudaMalloc(&bad, 2 * sizeof(unsigned long long)) != cudaSuccess) return VX_ECUDA;
+  cudaMemset(bad, 0, 2 * sizeof(unsigned long long));
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  exact_arith_kernel<<<sms * 8, 256>>>(n, seed, growth, bad);
+  unsigned long long h[2] = {0, 0};
+  const cudaError_t e = cudaMemcpy(h, bad, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(bad);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return VX_ECUDA;
+  if (sqrt_mismatches) *sqrt_mismatches = h[0];
+  if (div_mismatches) *div_mismatches = h[1];
+  return VX_OK;
+}
 
 extern "C" int vx_probe_pipe_rates(int device, double* dadd_per_s, double* fadd_per_s) {
   int prev = 0;
