@@ -73,6 +73,7 @@ struct FBox {
 struct __align__(16) WarpSmem {
   int W[kWcapD];       // brick list (gather slots), ascending site index
   int L[kLcapD];       // dense mode: a sub-brick's survivors (binned positions)
+  float4 bxy;          // the column's x/y box (c[0], c[1], h[0], h[1]), shared by its sub-bricks
   unsigned evals;      // exact evaluations the eval kernel will do for this warp's sub-bricks
 };
 
@@ -233,7 +234,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
     cc[a] = 0.5 * (blo[a] + bhi[a]);
     hs[a] = 0.5 * (bhi[a] - blo[a]);
   }
-  const long long nsbx = (g.n[0] + 7) / 8, nsby = (g.n[1] + 7) / 8;
+  const long long nsbx = g.nsbx, nsby = g.nsby;
   auto sb_id = [&](long long x, long long y, long long z) {  // 8x8x4 sub-brick at voxel (x, y, z)
     return (x >> 3) + nsbx * ((y >> 3) + nsby * ((z - g.z_begin) >> 2));
   };
@@ -353,6 +354,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
     }
   }
   if (tid == 0) S.n_kept = 0;
+  for (int k = tid; k < kTcap; k += kB2Threads) S.idx[k] = 0x7fffffff;  // sort padding
   if (tid < 2 * kSB + 16 * nbb) {  // exact voxel centres (geometry.hpp:58-60)
     const int a = tid < kSB ? 0 : (tid < 2 * kSB ? 1 : 2), k = tid - a * kSB;
     (a == 0 ? S.cx : a == 1 ? S.cy : S.cz)[k] = center(K0[a] + k, g.sp[a]);
@@ -419,8 +421,12 @@ __global__ void __launch_bounds__(kB2Threads, 4)
   if (T <= kTcap) {  // rank sort of the kept sites by site index (ties impossible)
     for (int f = tid; f < T; f += kB2Threads) {
       const int me = S.idx[f];
+      const int4* idx4 = reinterpret_cast<const int4*>(S.idx);  // padded with INT_MAX
       int rank = 0;
-      for (int k = 0; k < T; ++k) rank += S.idx[k] < me;
+      for (int k = 0; k < (T + 3) >> 2; ++k) {
+        const int4 v = idx4[k];
+        rank += (v.x < me) + (v.y < me) + (v.z < me) + (v.w < me);
+      }
       S.ord[rank] = (short)f;
     }
   }
@@ -478,6 +484,22 @@ __global__ void __launch_bounds__(kB2Threads, 4)
   bool col_any = false;
 #pragma unroll
   for (int b = 0; b < kMaxBB; ++b) col_any |= bval[b];
+  if (lane == 0) ws.bxy = make_float4(Bxy.c[0], Bxy.c[1], Bxy.h[0], Bxy.h[1]);
+  __syncwarp();
+  // a sub-brick's box: the column's x/y extent (every sub-brick of the column
+  // shares it) and its own z extent -- the values box_of would give
+  auto box_sub = [&](int z0, int nz) {
+    FBox B;
+    const float4 xy = ws.bxy;
+    B.c[0] = xy.x;
+    B.c[1] = xy.y;
+    B.h[0] = xy.z;
+    B.h[1] = xy.w;
+    const double l = S.cz[z0], h = S.cz[z0 + nz - 1];
+    B.c[2] = (float)(0.5 * (l + h) - cc[2]);
+    B.h[2] = (float)(0.5 * (h - l)) * (1.f + kRel) + 2.f * e_d;
+    return B;
+  };
   if (!col_any) return;  // no barrier follows
   if (cta_ok) {
     float myub[kMaxBB];
@@ -572,7 +594,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       // two passes over the brick list in chunks of 32: arg-min of the upper
       // bounds (the reference s0), then tau + bisector cull and compaction in
       // slot (= site index) order
-      const FBox Bs = box_of(bxo, sy, sz, sext[0], sext[1], sext[2]);
+      const FBox Bs = box_sub(sz, sext[2]);
       auto okey = [](float v) -> unsigned {
         const unsigned b = __float_as_uint(v);
         return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
@@ -633,7 +655,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
         if (ok) ws.evals += (unsigned)(n2 * sext[0] * sext[1] * sext[2]);
       }
     } else if (brick_ok) {
-      const FBox Bs = box_of(bxo, sy, sz, sext[0], sext[1], sext[2]);
+      const FBox Bs = box_sub(sz, sext[2]);
       // one bound evaluation per brick-list site, kept in registers (slots
       // lane and lane + 32; nW <= 64)
       const bool va = lane < nW, vb = lane + 32 < nW;
