@@ -122,6 +122,37 @@ extern "C" int vx_probe_exact_arith(int device, uint64_t n, uint64_t seed, doubl
   return VX_OK;
 }
 
+// H2D copy time of a host buffer through this library's runtime (diagnostics)
+extern "C" int vx_probe_h2d(int device, const void* host, uint64_t bytes, int use_null_stream, float* ms_out) {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess) return VX_ECUDA;
+  void* d = nullptr;
+  if (cudaMalloc(&d, bytes) != cudaSuccess) return VX_ECUDA;
+  cudaStream_t s = nullptr;
+  if (!use_null_stream) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    cudaEventRecord(e0, s);
+    cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, s);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (s) cudaStreamDestroy(s);
+  cudaFree(d);
+  cudaSetDevice(prev);
+  if (ms_out) *ms_out = best;
+  return cudaGetLastError() == cudaSuccess ? VX_OK : VX_ECUDA;
+}
+
 extern "C" int vx_probe_pipe_rates(int device, double* dadd_per_s, double* fadd_per_s) {
   int prev = 0;
   cudaGetDevice(&prev);

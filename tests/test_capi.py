@@ -153,9 +153,10 @@ def test_prune_rejects_voronoi():
 
 @pytest.mark.parametrize("where", [0, 123456, 299999])
 def test_large_site_set_validation_threads(where):
-    """The host position check is split over threads for large site sets; a
-    bad coordinate anywhere gives the reference's message (sites.cpp:54-57)
-    before any device work."""
+    """A bad coordinate anywhere gives the reference's message
+    (sites.cpp:54-57).  Without a device (this CPU suite) the host check
+    reports it; on a GPU the ingest kernel does, before any labelling work
+    (test_gpu_parity.py::test_device_validation_rejects_bad_positions)."""
     import numpy as np
 
     import paper_2201_13234_b200 as vx

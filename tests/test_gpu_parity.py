@@ -720,3 +720,26 @@ def test_sites_hugging_the_domain_faces(oracle_mod, kind, periodic):
     r = run_fast(p, prune=False)
     assert np.array_equal(r.labels.labels, lab), int((r.labels.labels != lab).sum())
     assert np.array_equal(bits(r.distances.values), bits(dist))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("where", [0, 123456, 299999])
+@pytest.mark.parametrize("bad", [1.0, 0.0, float("nan"), 1.5, -1e-300, float("inf")])
+def test_device_validation_rejects_bad_positions(where, bad):
+    """Host-buffer calls validate the positions on the device during ingest
+    (sites.cpp:54-57: finite and strictly inside the domain) and fail with
+    the reference's message before any labelling work; the context stays
+    usable for the next call."""
+    import paper_2201_13234_b200 as vx
+
+    n = 300000
+    pos = np.random.default_rng(5).uniform(0.01, 0.99, 3 * n)
+    box = vx.Domain([1.0, 1.0, 1.0], vx.Boundary.Periodic)
+    grid = vx.VoxelGrid([32, 32, 32], box)
+    good = vx.tessellate_fast(vx.SiteSet(vx.Kind.Voronoi, 3, pos.copy(), None, 0.0), grid, distances=False)
+    pos[3 * where + 2] = bad
+    with pytest.raises(ValueError, match="site positions must lie strictly inside the domain"):
+        vx.tessellate_fast(vx.SiteSet(vx.Kind.Voronoi, 3, pos, None, 0.0), grid)
+    pos[3 * where + 2] = 0.5
+    again = vx.tessellate_fast(vx.SiteSet(vx.Kind.Voronoi, 3, pos, None, 0.0), grid, distances=False)
+    assert again.labels.labels.shape == good.labels.labels.shape
