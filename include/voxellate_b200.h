@@ -208,6 +208,9 @@ int vx_probe_pipe_rates(int device, double* dadd_per_s, double* fadd_per_s);
  * writes the number of bitwise mismatches of each. */
 int vx_probe_exact_arith(int device, uint64_t n, uint64_t seed, double growth,
                          uint64_t* sqrt_mismatches, uint64_t* div_mismatches);
+/* Best-of-3 device time (ms) of one host->device copy of `bytes` from `host`
+ * through this library's runtime (diagnostics of the end-to-end number). */
+int vx_probe_h2d(int device, const void* host, uint64_t bytes, int use_null_stream, float* ms_out);
 
 #ifdef __cplusplus
 }

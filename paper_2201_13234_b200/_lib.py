@@ -114,6 +114,7 @@ SIGNATURES = {
     "vx_probe_pipe_rates": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "vx_probe_exact_arith": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_double, C.POINTER(C.c_uint64),
                                        C.POINTER(C.c_uint64)]),
+    "vx_probe_h2d": (C.c_int, [C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_float)]),
     "vx_tessellate_to_files": (C.c_int, [_P, C.POINTER(vx_problem), C.POINTER(vx_options), C.c_char_p,
                                          C.c_char_p, C.c_int64, C.POINTER(vx_stats)]),
     "vx_write_image": (C.c_int, [C.c_char_p, C.c_int, C.c_int, _P, _P, C.c_int, C.c_int, C.c_int64,

@@ -35,8 +35,6 @@ import ctypes as C  # noqa: E402
 from paper_2201_13234_b200._lib import lib  # noqa: E402
 
 L = lib()
-L.vx_probe_h2d.restype = C.c_int
-L.vx_probe_h2d.argtypes = [C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_float)]
 for label, arr in (("pinned", pin_t.numpy()), ("pageable", np.array(p.positions))):
     for ns in (0, 1):
         ms = C.c_float(0)
