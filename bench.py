@@ -267,13 +267,14 @@ def run_ours(args):
         sites_h = vx.SiteSet(sites.kind, 3, pin_pos.numpy(), None if sites.times is None else
                              torch.from_numpy(sites.times).pin_memory().numpy(), sites.growth)
         out = torch.empty(nvs, dtype=torch.int32).pin_memory().numpy()
+        hist_h = torch.zeros(ns, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
         e2e_t = []
         for k in range(1 + args.e2e_steps):
             if dist is not None:
                 dist.barrier()
             t0 = time.perf_counter()
             r = vx.tessellate_fast(sites_h, grid, distances=False, histogram=True, slab=(zb, ze),
-                                   device=dev, out=out)
+                                   device=dev, out=out, histogram_out=hist_h)
             e2e_t.append(time.perf_counter() - t0)
         t_e2e = torch.tensor([float(np.mean(e2e_t[1:]))], dtype=torch.float64, device=f"cuda:{dev}")
         if dist is not None:

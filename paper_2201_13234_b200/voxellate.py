@@ -237,7 +237,7 @@ def _problem(sites: SiteSet, grid: VoxelGrid) -> vx_problem:
 
 def _run(engine: str, sites: SiteSet, grid: VoxelGrid, options: Optional[FastOptions],
          distances: bool, histogram: bool, slab, device, ball_scale, context=None, out=None,
-         profile=False, n_gpus=None) -> TessResult:
+         profile=False, n_gpus=None, histogram_out=None) -> TessResult:
     P = _problem(sites, grid)
     O = vx_options()
     lib().vx_options_init(C.byref(O))
@@ -264,7 +264,12 @@ def _run(engine: str, sites: SiteSet, grid: VoxelGrid, options: Optional[FastOpt
         labels = np.empty(nvs, dtype=np.int32)
     O.profile_stages = 1 if profile else 0
     dist = np.empty(nvs, dtype=np.float64) if distances else None
-    hist = np.zeros(sites.count(), dtype=np.uint64) if histogram else None
+    if histogram_out is not None:  # caller-provided (e.g. pinned) histogram buffer
+        hist = histogram_out.reshape(-1).view(np.uint64)
+        if hist.size != sites.count() or not hist.flags.c_contiguous:
+            raise ValueError("histogram_out must be a contiguous buffer of one count per site")
+    else:
+        hist = np.zeros(sites.count(), dtype=np.uint64) if histogram else None
     O.distances_out = _ptr(dist)
     O.histogram_out = _ptr(hist)
     st = vx_stats()
@@ -279,13 +284,15 @@ def _run(engine: str, sites: SiteSet, grid: VoxelGrid, options: Optional[FastOpt
 
 def tessellate_fast(sites: SiteSet, grid: VoxelGrid, options: Optional[FastOptions] = None, *,
                     distances: bool = True, histogram: bool = False, slab=None, device=None,
-                    ball_scale=None, context=None, out=None, profile=False, n_gpus=None) -> TessResult:
+                    ball_scale=None, context=None, out=None, profile=False, n_gpus=None,
+                    histogram_out=None) -> TessResult:
     """Two-step engine on the GPU (tessellate.cpp:195-282).  ``slab=(z0, z1)``
     labels only last-axis planes [z0, z1) (the multi-GPU decomposition);
-    ``out`` receives the labels (e.g. a pinned host buffer); ``n_gpus`` splits
-    the call over that many devices from one process."""
+    ``out`` / ``histogram_out`` receive the labels / grain volumes (e.g. pinned
+    host buffers; the latter implies ``histogram``); ``n_gpus`` splits the call
+    over that many devices from one process."""
     return _run("fast", sites, grid, options or FastOptions(), distances, histogram, slab, device,
-                ball_scale, context, out, profile, n_gpus)
+                ball_scale, context, out, profile, n_gpus, histogram_out)
 
 
 def tessellate_brute(sites: SiteSet, grid: VoxelGrid, *, distances: bool = True,

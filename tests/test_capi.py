@@ -169,3 +169,14 @@ def test_large_site_set_validation_threads(where):
     sites = vx.SiteSet(vx.Kind.Voronoi, 3, pos, None, 0.0)
     with pytest.raises(ValueError, match="site positions must lie strictly inside the domain"):
         vx.tessellate_fast(sites, grid)
+
+
+def test_histogram_out_must_match_site_count():
+    import numpy as np
+
+    import paper_2201_13234_b200 as vx
+
+    box, s = _sites(kind=0, d=2, n=5)
+    grid = vx.VoxelGrid([8, 8], box)
+    with pytest.raises(ValueError, match="histogram_out"):
+        vx.tessellate_fast(s, grid, histogram_out=np.zeros(4, dtype=np.uint64))

@@ -743,3 +743,23 @@ def test_device_validation_rejects_bad_positions(where, bad):
     pos[3 * where + 2] = 0.5
     again = vx.tessellate_fast(vx.SiteSet(vx.Kind.Voronoi, 3, pos, None, 0.0), grid, distances=False)
     assert again.labels.labels.shape == good.labels.labels.shape
+
+
+@pytest.mark.gpu
+def test_caller_buffers_for_labels_and_histogram():
+    """out= / histogram_out= (e.g. pinned buffers) receive exactly what the
+    default call returns."""
+    import torch
+
+    import oracle
+    import paper_2201_13234_b200 as vx
+
+    p = oracle.baseline_config(1)
+    sites, grid = to_vx(p)
+    ref = vx.tessellate_fast(sites, grid, distances=False, histogram=True)
+    out = torch.empty(p.n_voxels, dtype=torch.int32).pin_memory().numpy()
+    hist = torch.zeros(p.n_sites, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    hist[:] = 7  # the call overwrites every count
+    r = vx.tessellate_fast(sites, grid, distances=False, out=out, histogram_out=hist)
+    assert np.array_equal(out.view(np.uint32), ref.labels.labels)
+    assert np.array_equal(hist, ref.histogram) and np.shares_memory(r.histogram, hist)
