@@ -763,3 +763,22 @@ def test_caller_buffers_for_labels_and_histogram():
     r = vx.tessellate_fast(sites, grid, distances=False, out=out, histogram_out=hist)
     assert np.array_equal(out.view(np.uint32), ref.labels.labels)
     assert np.array_equal(hist, ref.histogram) and np.shares_memory(r.histogram, hist)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("counts", [[64, 1, 64], [1, 1, 200], [1, 64, 1], [96, 80, 1], [1, 40, 56], [3, 2, 1]])
+@pytest.mark.parametrize("kind,periodic", [(0, True), (1, False), (2, True), (0, False)])
+def test_single_voxel_axes_in_3d(oracle_mod, counts, kind, periodic):
+    """3-D grids with one voxel along some axes (a slice or a line through a
+    3-D site set): sub-bricks and super-bricks are mostly outside the grid and
+    the voxel centre sits mid-domain on the thin axes."""
+    rng = np.random.default_rng(sum(counts) * 7 + kind)
+    L = rng.uniform(0.5, 2.0, 3)
+    ns = int(rng.integers(20, 300))
+    pos, t = oracle_mod.generate_uniform_sites(3, L, ns, kind, float(0.5 * np.prod(L) ** (1 / 3) / ns ** (1 / 3)),
+                                               int(rng.integers(1 << 40)))
+    p = oracle_mod.Problem(kind, counts, L, periodic, pos, t, [0.0, 1.3, 0.8][kind])
+    lab, dist = oracle_mod.brute(p)
+    r = run_fast(p, prune=False)
+    assert np.array_equal(r.labels.labels, lab)
+    assert np.array_equal(bits(r.distances.values), bits(dist))
