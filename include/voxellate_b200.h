@@ -68,7 +68,7 @@ typedef struct vx_options {
   double override_param;
   int32_t device;         /* CUDA ordinal; -1 = the context's device */
   int32_t device_pointers;/* 1: positions/times/weights and all outputs are device pointers */
-  void* stream;           /* cudaStream_t to run on; NULL = the context's stream */
+  void* stream;           /* cudaStream_t to run on; NULL = the context's stream (pass cudaStreamLegacy, 0x1, for the legacy default stream) */
   int32_t asynchronous;   /* 1: return after enqueueing (device_pointers only; stats
                              then carry no device-side counts) */
   int32_t profile_stages; /* 1: record CUDA events around each stage -> stats.stage_ms */
@@ -130,6 +130,10 @@ int vx_context_create(int device, vx_context** out);
 void vx_context_destroy(vx_context* ctx);
 /* device workspace bytes currently held by the context */
 int64_t vx_context_workspace_bytes(const vx_context* ctx);
+/* stage times (ms, the vx_stats.stage_ms layout) of the context's last call
+ * with options.profile_stages -- also asynchronous calls and CUDA-graph
+ * replays of a captured call; waits for that work to finish */
+int vx_context_stage_ms(vx_context* ctx, float* stage_ms);
 
 /* ---- engines ---- */
 /* tessellate_fast (tessellate.cpp:195-282): labels_out holds N_v (or slab) int32.

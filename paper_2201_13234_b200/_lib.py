@@ -98,6 +98,7 @@ SIGNATURES = {
     "vx_context_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "vx_context_destroy": (None, [_P]),
     "vx_context_workspace_bytes": (C.c_int64, [_P]),
+    "vx_context_stage_ms": (C.c_int, [_P, C.POINTER(C.c_float)]),
     "vx_tessellate": (C.c_int, [_P, C.POINTER(vx_problem), C.POINTER(vx_options), _P,
                                 C.POINTER(vx_stats)]),
     "vx_tessellate_brute": (C.c_int, [_P, C.POINTER(vx_problem), C.POINTER(vx_options), _P,

@@ -66,6 +66,7 @@ struct vx_context {
   DevParams* h_prm = nullptr;
   DevCounters* h_ctr = nullptr;
   cudaEvent_t ev[8] = {};  // stage markers (options.profile_stages)
+  bool ev_marked[8] = {};  // which markers the last profiled call recorded
   cudaStream_t copy_stream = nullptr;  // chunked D2H of host-buffer calls
   cudaEvent_t chunk_ev[16] = {};
   std::vector<cudaEvent_t> sink_ev;    // vx_tessellate_to_files: one per chunk
@@ -116,7 +117,13 @@ struct StageTimer {
   bool marked[8] = {};
   void mark(int i) {
     if (on) {
-      cudaEventRecord(ev[i], st);
+      // under stream capture an External record becomes an event-record node
+      // of the graph (a plain record would only order the capture); the flag
+      // is invalid outside a capture
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cs);
+      if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal);
+      else cudaEventRecord(ev[i], st);
       marked[i] = true;
     }
   }
@@ -587,7 +594,9 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
   bool labels_copied = false;  // chunked D2H already issued
   std::vector<SinkChunk> sink_chunks;
   try {
-    tm.on = O.profile_stages && !O.asynchronous;
+    // asynchronous calls (and CUDA-graph captures of them) record the stage
+    // markers too; vx_context_stage_ms reads them once the work has run
+    tm.on = O.profile_stages != 0;
     tm.st = st;
     tm.ev = ctx->ev;
     if (tm.on && !ctx->ev[0])
@@ -822,6 +831,8 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       stats->n_voxels = nvs;
       stats->param = std::numeric_limits<double>::quiet_NaN();
     }
+    if (tm.on)
+      for (int i = 0; i < 8; ++i) ctx->ev_marked[i] = tm.marked[i];
     if (O.asynchronous) return VX_OK;
     ck(cudaMemcpyAsync(ctx->h_prm, prm, sizeof(DevParams), cudaMemcpyDeviceToHost, st), "D2H params");
     ck(cudaMemcpyAsync(ctx->h_ctr, ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st), "D2H counters");
@@ -1023,6 +1034,25 @@ void vx_context_destroy(vx_context* ctx) {
       if (e) cudaEventDestroy(e);
   }
   delete ctx;
+}
+
+int vx_context_stage_ms(vx_context* ctx, float* stage_ms) {
+  if (!ctx || !stage_ms) return fail(VX_EINVAL, "context and stage_ms must not be NULL");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  DeviceGuard guard(ctx->device);
+  for (int i = 0; i < 8; ++i) stage_ms[i] = 0.f;
+  int last = -1;
+  for (int i = 0; i < 8; ++i)
+    if (ctx->ev_marked[i]) last = i;
+  if (last < 0) return VX_OK;
+  cudaError_t e = cudaEventSynchronize(ctx->ev[last]);
+  if (e != cudaSuccess) return fail(VX_ECUDA, std::string("stage events: ") + cudaGetErrorString(e));
+  for (int i = 0; i < 7; ++i)
+    if (ctx->ev_marked[i] && ctx->ev_marked[i + 1]) {
+      e = cudaEventElapsedTime(&stage_ms[i], ctx->ev[i], ctx->ev[i + 1]);
+      if (e != cudaSuccess) return fail(VX_ECUDA, std::string("stage events: ") + cudaGetErrorString(e));
+    }
+  return VX_OK;
 }
 
 int64_t vx_context_workspace_bytes(const vx_context* ctx) {

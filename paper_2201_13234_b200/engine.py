@@ -32,6 +32,15 @@ class Tessellator:
         except Exception:
             pass
 
+    def stage_ms(self) -> dict:
+        """Stage times of the last profiled call on this context (including an
+        asynchronous call or a replay of a captured one), once it has run."""
+        from ._lib import STAGES
+
+        ms = (C.c_float * 8)()
+        check(lib().vx_context_stage_ms(self._ctx, ms))
+        return {name: float(ms[i]) for i, name in enumerate(STAGES)}
+
     @property
     def workspace_bytes(self) -> int:
         return int(lib().vx_context_workspace_bytes(self._ctx))
@@ -64,7 +73,10 @@ class Tessellator:
             O.has_override = 1
             O.override_param = float(override)
         if stream is not None:
-            O.stream = C.c_void_p(stream)
+            # torch's default stream has handle 0, which the C-ABI reads as "the
+            # context's own stream": pass cudaStreamLegacy (0x1) instead, so the
+            # work is ordered with the caller's events and kernels on it
+            O.stream = C.c_void_p(stream if stream else 1)
         O.asynchronous = 1 if asynchronous else 0
         O.profile_stages = 1 if profile else 0
         if slab is not None:
@@ -79,3 +91,25 @@ class Tessellator:
         check(lib().vx_tessellate(self._ctx, C.byref(P), C.byref(O), C.c_void_p(labels.data_ptr()),
                                   C.byref(st)))
         return stats_dict(st)
+
+    def capture(self, *, warmup: bool = True, **run_kwargs):
+        """Capture one asynchronous call into a CUDA graph (torch.cuda.CUDAGraph)
+        and return it: ``graph.replay()`` re-labels the same buffers -- e.g.
+        after the caller rewrote ``positions`` in place -- with one launch
+        instead of the call's ~15 kernel / memset launches.  Shapes, options
+        and buffer addresses are frozen at capture; the workspaces were sized
+        by the warm-up call.  Device-pointer calls only."""
+        import torch
+
+        run_kwargs.pop("stream", None)
+        run_kwargs.pop("asynchronous", None)
+        s = torch.cuda.Stream(device=self.device)
+        with torch.cuda.device(self.device):
+            if warmup:  # sizes every workspace and sets the kernel attributes outside the capture
+                with torch.cuda.stream(s):
+                    self.run(stream=s.cuda_stream, **run_kwargs)
+                s.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                self.run(stream=s.cuda_stream, asynchronous=True, **run_kwargs)
+        return g

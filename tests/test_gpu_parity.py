@@ -782,3 +782,37 @@ def test_single_voxel_axes_in_3d(oracle_mod, counts, kind, periodic):
     r = run_fast(p, prune=False)
     assert np.array_equal(r.labels.labels, lab)
     assert np.array_equal(bits(r.distances.values), bits(dist))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [1, 4])
+def test_cuda_graph_replay_relabels_moved_sites(oracle_mod, cfg):
+    """A device-pointer call captured into a CUDA graph (Tessellator.capture):
+    replaying it after rewriting the positions in place gives exactly what a
+    fresh call gives for the new sites -- the whole pipeline (binning, t0
+    search, ball phase, shell, histogram) lives in the graph."""
+    import torch
+
+    from paper_2201_13234_b200.engine import Tessellator
+
+    p = oracle_mod.baseline_config(cfg)
+    eng = Tessellator(0)
+    pos = torch.from_numpy(p.positions.copy()).cuda()
+    t = torch.from_numpy(p.times.copy()).cuda() if p.times is not None else None
+    lab = torch.empty(p.n_voxels, dtype=torch.int32, device="cuda")
+    hist = torch.zeros(p.n_sites, dtype=torch.int64, device="cuda")
+    kw = dict(kind=p.kind, counts=list(p.counts), lengths=list(p.lengths), periodic=p.periodic,
+              positions=pos, times=t, growth=p.growth, labels=lab, histogram=hist)
+    g = eng.capture(**kw)
+    rng = np.random.default_rng(cfg)
+    for trial in range(3):
+        new = rng.uniform(0.001, 0.999, p.positions.size) * np.tile(np.asarray(p.lengths), p.n_sites)
+        pos.copy_(torch.from_numpy(new))
+        hist.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        q = oracle_mod.Problem(p.kind, p.counts, p.lengths, p.periodic, new, p.times, p.growth)
+        ref = run_fast(q, distances=False, histogram=True)
+        assert np.array_equal(lab.cpu().numpy().view(np.uint32), ref.labels.labels)
+        assert np.array_equal(hist.cpu().numpy().astype(np.uint64), ref.histogram)
+    eng.close()
