@@ -257,6 +257,8 @@ def _run(engine: str, sites: SiteSet, grid: VoxelGrid, options: Optional[FastOpt
     plane = grid.voxel_count() // grid.counts[-1]
     nvs = plane * (ze - zb)
     if out is not None:  # caller-provided (e.g. pinned) label buffer
+        if out.dtype not in (np.int32, np.uint32):
+            raise ValueError("out must hold int32 or uint32 labels")
         labels = out.reshape(-1).view(np.int32)
         if labels.size != nvs or not labels.flags.c_contiguous:
             raise ValueError("out must be a contiguous buffer of the labelled voxel count")
@@ -265,6 +267,8 @@ def _run(engine: str, sites: SiteSet, grid: VoxelGrid, options: Optional[FastOpt
     O.profile_stages = 1 if profile else 0
     dist = np.empty(nvs, dtype=np.float64) if distances else None
     if histogram_out is not None:  # caller-provided (e.g. pinned) histogram buffer
+        if histogram_out.dtype not in (np.uint64, np.int64):
+            raise ValueError("histogram_out must hold uint64 or int64 counts")
         hist = histogram_out.reshape(-1).view(np.uint64)
         if hist.size != sites.count() or not hist.flags.c_contiguous:
             raise ValueError("histogram_out must be a contiguous buffer of one count per site")

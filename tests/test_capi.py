@@ -180,3 +180,16 @@ def test_histogram_out_must_match_site_count():
     grid = vx.VoxelGrid([8, 8], box)
     with pytest.raises(ValueError, match="histogram_out"):
         vx.tessellate_fast(s, grid, histogram_out=np.zeros(4, dtype=np.uint64))
+
+
+def test_caller_buffers_dtype_checked():
+    import numpy as np
+
+    import paper_2201_13234_b200 as vx
+
+    box, s = _sites(kind=0, d=2, n=5)
+    grid = vx.VoxelGrid([8, 8], box)
+    with pytest.raises(ValueError, match="histogram_out"):
+        vx.tessellate_fast(s, grid, histogram_out=np.zeros(5, dtype=np.float64))
+    with pytest.raises(ValueError, match="out must hold"):
+        vx.tessellate_fast(s, grid, out=np.zeros(64, dtype=np.float32))
