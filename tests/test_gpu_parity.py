@@ -816,3 +816,22 @@ def test_cuda_graph_replay_relabels_moved_sites(oracle_mod, cfg):
         assert np.array_equal(lab.cpu().numpy().view(np.uint32), ref.labels.labels)
         assert np.array_equal(hist.cpu().numpy().astype(np.uint64), ref.histogram)
     eng.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", [0, 1])
+def test_unresolved_list_overflow_path(oracle_mod, kind):
+    """More unresolved voxels than the unresolved list holds (2^22): with a
+    vanishing ball every voxel of a 4.8e6-voxel grid goes to the shell search,
+    which then finds them by their -1 sentinel in the label image."""
+    rng = np.random.default_rng(4242 + kind)
+    counts = [200, 200, 120]
+    L = np.array([1.0, 1.0, 0.6])
+    pos, t = oracle_mod.generate_uniform_sites(3, L, 150, kind, 0.05, int(rng.integers(1 << 40)))
+    p = oracle_mod.Problem(kind, counts, L, True, pos, t, [0.0, 1.0][kind])
+    override = 1e-9 if kind == 0 else float(np.min(t))
+    r = run_fast(p, prune=False, override=override)
+    assert r.stats["n_unresolved"] == p.n_voxels > (1 << 22)
+    lab, dist = oracle_mod.brute(p)
+    assert np.array_equal(r.labels.labels, lab)
+    assert np.array_equal(bits(r.distances.values), bits(dist))
