@@ -1012,13 +1012,26 @@ long long ball12_subbricks(const Geo& g) {
 // Dense mode when the mean site spacing is below ~8.5 voxels (on the finest
 // true axis): an 8^3 brick then sees more than ~60 sites (VX_DENSE=0/1 forces).
 bool ball12_dense(const Geo& g) {
-  static const int env = std::getenv("VX_DENSE") ? std::atoi(std::getenv("VX_DENSE")) : -1;
+  const char* ev = std::getenv("VX_DENSE");  // read per call: tests switch it
+  const int env = ev ? std::atoi(ev) : -1;
   if (env == 0 || env == 1) return env == 1;
   double sp = 1e300;
   for (int a = 0; a < 3; ++a)
     if (g.n[a] > 1) sp = std::min(sp, g.sp[a]);
   const double spacing = pow(g.vol_true / (double)(g.n_sites > 0 ? g.n_sites : 1), 1.0 / g.dim);
-  return sp < 1e300 && spacing < 8.5 * sp;
+  if (sp < 1e300 && spacing < 8.5 * sp) return true;
+  if (g.dim != 3) return false;
+  // anisotropic voxels: expected sites reaching an 8 x 8 x 4 sub-brick from its
+  // physical extents (+ ~1.2 site spacings of reach per axis); thick slices
+  // make it elongated and its lists long at moderate density.  Measured on
+  // 512^2 x (512 / r) with 10-voxel in-plane spacing (scripts/aniso_check.py):
+  // dense mode wins from r ~ 3 (this estimate 9.5) on -- r = 4: 26 -> 50, r = 8:
+  // 5.5 -> 29 Gvox/s -- and loses below (r = 2, estimate 8.0: 88 vs 73).
+  const double lambda = (double)g.n_sites / g.vol_true;
+  const double ext[3] = {8.0 * g.sp[0], 8.0 * g.sp[1], 4.0 * g.sp[2]};
+  double e = lambda;
+  for (int a = 0; a < 3; ++a) e *= ext[a] + 1.2 * spacing;
+  return e > 9.5;
 }
 
 template <int KIND, bool PER, bool DENSE>

@@ -479,15 +479,18 @@ def test_large_random_vs_reference_library(i):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("case", ["flat_periodic", "tall_nonperiodic", "dense_jm", "flat_laguerre"])
-def test_overflow_subbrick_shell_vs_reference(case):
+def test_overflow_subbrick_shell_vs_reference(case, monkeypatch):
     """Strongly anisotropic voxels / very dense sites overflow the ball phase's
     brick caps; those sub-bricks are labelled by the sub-brick shell search.
-    Bit-exact against the reference library, and the path is really taken."""
+    Bit-exact against the reference library, and the path is really taken
+    (standard lists forced: the default would pick dense mode for several of
+    these and not overflow; test_dense_mode_vs_reference covers that)."""
     import oracle
     import paper_2201_13234_b200 as vx
 
     if not oracle.have_ref():
         pytest.skip("oracle/_ref not built")
+    monkeypatch.setenv("VX_DENSE", "0")
     kind, counts, ns, per = {"flat_periodic": (0, [512, 512, 8], 20000, True),
                              "tall_nonperiodic": (0, [32, 32, 2048], 8000, False),
                              "dense_jm": (1, [96, 96, 96], 40000, True),
@@ -835,3 +838,28 @@ def test_unresolved_list_overflow_path(oracle_mod, kind):
     lab, dist = oracle_mod.brute(p)
     assert np.array_equal(r.labels.labels, lab)
     assert np.array_equal(bits(r.distances.values), bits(dist))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ratio,kind", [(3.0, 0), (4.0, 1), (6.0, 2), (8.0, 0)])
+def test_thick_slices_take_dense_lists_vs_reference(ratio, kind):
+    """Voxels `ratio` times thicker along z than in-plane at moderate density
+    (~10 in-plane voxels between sites): the anisotropy-aware choice takes the
+    dense lists instead of overflowing to the shell searches; bit-exact against
+    the reference library, and no sub-brick overflows."""
+    import oracle
+    import paper_2201_13234_b200 as vx
+
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    nxy, nz = 128, int(round(128 / ratio))
+    L = np.array([1.0, 1.0, 1.0])
+    ns = int(nxy * nxy * nz * ratio / 1000)
+    pos, t = oracle.generate_uniform_sites(3, L, ns, kind, 0.5 / ns ** (1 / 3), 31 + kind)
+    p = oracle.Problem(kind, [nxy, nxy, nz], L, True, pos, t, 0.0 if kind == 0 else 1.1)
+    lab_ref, dist_ref, _, _ = oracle.ref_tessellate(p)
+    sites, grid = to_vx(p)
+    r = vx.tessellate_fast(sites, grid, distances=True, histogram=True)
+    assert r.stats["overflow_bricks"] == 0
+    assert np.array_equal(r.labels.labels, lab_ref), int((r.labels.labels != lab_ref).sum())
+    assert np.array_equal(r.distances.values.view(np.uint64), dist_ref.view(np.uint64))
