@@ -863,3 +863,40 @@ def test_thick_slices_take_dense_lists_vs_reference(ratio, kind):
     assert r.stats["overflow_bricks"] == 0
     assert np.array_equal(r.labels.labels, lab_ref), int((r.labels.labels != lab_ref).sum())
     assert np.array_equal(r.distances.values.view(np.uint64), dist_ref.view(np.uint64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", [0, 1, 2])
+@pytest.mark.parametrize("n", [16, 24, 40])
+def test_half_period_offsets(oracle_mod, kind, n):
+    """Periodic boxes with a handful of sites on voxel centres, so many
+    site-voxel offsets are exactly +-L/2 (floor(u/L + 0.5) rounds up at the
+    half-tie, geometry.hpp:82-89; test_geometry.cpp:42-48) and images of the
+    same site tie with each other: the kernels' 0.49 L fast path and the
+    wrapped slow path must agree with the reference's formula everywhere."""
+    rng = np.random.default_rng(n * 3 + kind)
+    L = np.array([1.0, 0.5, 2.0])  # dyadic spacings for n = 16 (and exact halves)
+    counts = [n, n, n]
+    sp = L / np.array(counts)
+    ns = 6
+    k = rng.integers(0, n, (ns, 3))
+    pos = ((k + 0.5) * sp).reshape(-1)
+    t = rng.choice([0.0, 0.25], ns) if kind else None
+    p = oracle_mod.Problem(kind, counts, L, True, pos, t, [0.0, 1.0, 0.5][kind])
+    lab, dist = oracle_mod.brute(p)
+    for prune in (False, True):
+        if prune and kind == 0:
+            continue
+        r = run_fast(p, prune=prune)
+        if prune:  # the reference labels the prune survivors
+            dropped = oracle_mod.prune(p)
+            if dropped.any():
+                keep = np.nonzero(dropped == 0)[0]
+                q = oracle_mod.Problem(kind, counts, L, True, p.positions.reshape(-1, 3)[keep].reshape(-1),
+                                       p.times[keep], p.growth)
+                l2, d2 = oracle_mod.brute(q)
+                assert np.array_equal(r.labels.labels, keep[l2].astype(np.uint32))
+                assert np.array_equal(bits(r.distances.values), bits(d2))
+                continue
+        assert np.array_equal(r.labels.labels, lab), int((r.labels.labels != lab).sum())
+        assert np.array_equal(bits(r.distances.values), bits(dist))
