@@ -900,3 +900,27 @@ def test_half_period_offsets(oracle_mod, kind, n):
                 continue
         assert np.array_equal(r.labels.labels, lab), int((r.labels.labels != lab).sum())
         assert np.array_equal(bits(r.distances.values), bits(dist))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("periodic", [True, False])
+@pytest.mark.parametrize("sigma,growth", [(0.3, 1.0), (0.9, 1.0), (0.9, 2.5)])
+def test_polydisperse_laguerre_spheres(oracle_mod, periodic, sigma, growth):
+    """Laguerre from sphere packs (sites.cpp:87-104, t = -(r r)/G: negative
+    birth times and proximities), lognormal radii up to very polydisperse --
+    many sites are dominated and pruned (sites.cpp:113-171) and the survivors
+    are remapped to original indices (tessellate.cpp:274-280)."""
+    pos, radii = oracle_mod.generate_lognormal_spheres(600, 0.04, sigma, 1234 + int(10 * sigma))
+    t = oracle_mod.spheres_to_timed(radii, growth)
+    p = oracle_mod.Problem(2, [72, 64, 80], [1.0, 1.0, 1.0], periodic, pos, t, growth)
+    lab_all, dist_all = oracle_mod.brute(p)
+    dropped = oracle_mod.prune(p)
+    keep = np.nonzero(dropped == 0)[0]
+    q = oracle_mod.Problem(2, p.counts, p.lengths, periodic, pos.reshape(-1, 3)[keep].reshape(-1), t[keep], growth)
+    l2, d2 = oracle_mod.brute(q)
+    for prune, (lab, dist) in ((False, (lab_all, dist_all)), (True, (keep[l2].astype(np.uint32), d2))):
+        r = run_fast(p, prune=prune)
+        assert np.array_equal(r.labels.labels, lab), int((r.labels.labels != lab).sum())
+        assert np.array_equal(bits(r.distances.values), bits(dist))
+    if sigma > 0.5:
+        assert dropped.any()  # the pruning path is exercised
