@@ -6,6 +6,7 @@
 // stable LSD radix sort, so each cell -- and each x-row of cells -- is a
 // contiguous, ascending-site-index range of the SoA arrays bx/by/bz/bt/bidx.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "vx_internal.cuh"
 
@@ -48,7 +49,7 @@ __device__ __forceinline__ int cell_of(double v, double inv_cw, int m) {
 
 __global__ void keys_kernel(Geo g, const double* __restrict__ p3, const double* __restrict__ t,
                             const uint8_t* __restrict__ dropped, unsigned* __restrict__ keys,
-                            int* __restrict__ vals, DevParams* prm) {
+                            int* __restrict__ vals, int* __restrict__ counts, DevParams* prm) {
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   bool alive = false;
   double tv = 0.0;
@@ -61,6 +62,7 @@ __global__ void keys_kernel(Geo g, const double* __restrict__ p3, const double* 
       const int cz = cell_of(p3[3 * s + 2], g.inv_cw[2], g.m[2]);
       key = (unsigned)(cx + (long long)g.m[0] * (cy + (long long)g.m[1] * cz));
       if (t) tv = t[s];
+      atomicAdd(&counts[key], 1);  // sites per cell; their exclusive scan is cell_start
     }
     keys[s] = key;
     vals[s] = (int)s;
@@ -83,8 +85,10 @@ __global__ void gather_kernel(long long n, const int* __restrict__ vals,
                               const double* __restrict__ p3, const double* __restrict__ t,
                               double* __restrict__ bx, double* __restrict__ by,
                               double* __restrict__ bz, double* __restrict__ bt,
-                              int* __restrict__ bidx, float4* __restrict__ f4) {
+                              int* __restrict__ bidx, float4* __restrict__ f4,
+                              const int* __restrict__ cell_start, long long n_cells, DevCounters* ctr) {
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p == 0) ctr->n_alive = (unsigned long long)cell_start[n_cells];  // dropped sites sort last
   if (p >= n) return;
   const int s = vals[p];
   const double x = p3[3 * (long long)s + 0], y = p3[3 * (long long)s + 1],
@@ -98,31 +102,18 @@ __global__ void gather_kernel(long long n, const int* __restrict__ vals,
   if (f4) f4[p] = make_float4((float)x, (float)y, (float)z, (float)tv);
 }
 
-__global__ void cell_start_kernel(long long n, long long n_cells, const unsigned* __restrict__ keys,
-                                  int* __restrict__ cell_start, DevCounters* ctr) {
-  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (c > n_cells) return;
-  long long lo = 0, hi = n;  // first p with keys[p] >= c
-  while (lo < hi) {
-    const long long mid = (lo + hi) >> 1;
-    if (keys[mid] < (unsigned)c) lo = mid + 1;
-    else hi = mid;
-  }
-  cell_start[c] = (int)lo;
-  if (c == n_cells) ctr->n_alive = (unsigned long long)lo;
-}
-
 static int key_bits(long long n_cells) {
   int b = 1;
   while ((1ll << b) <= n_cells) ++b;
   return b;
 }
 
-size_t bin_tmp_bytes(long long n_sites) {
-  size_t bytes = 0;
+size_t bin_tmp_bytes(long long n_sites, long long n_cells) {
+  size_t bytes = 0, scan = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned*)nullptr, (unsigned*)nullptr,
                                   (int*)nullptr, (int*)nullptr, (int)n_sites, 0, 32);
-  return bytes;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan, (int*)nullptr, (int*)nullptr, (int)(n_cells + 1));
+  return bytes > scan ? bytes : scan;
 }
 
 int launch_ingest(const Geo& g, const Len16& len, int dim_in, const double* pos_in,
@@ -141,16 +132,21 @@ int launch_bin(const Geo& g, const double* p3, const double* t, const uint8_t* d
                cudaStream_t st) {
   const int T = 256;
   const unsigned nb = (unsigned)((g.n_sites + T - 1) / T);
-  keys_kernel<<<nb, T, 0, st>>>(g, p3, t, dropped, keys_a, vals_a, prm);
-  size_t bytes = cub_tmp_bytes;
-  const cudaError_t e = cub::DeviceRadixSort::SortPairs(cub_tmp, bytes, keys_a, keys_b, vals_a,
-                                                        vals_b, (int)g.n_sites, 0,
-                                                        key_bits(g.n_cells), st);
+  // cell_start = exclusive scan of the per-cell site counts (counted in place)
+  cudaError_t e = cudaMemsetAsync(cell_start, 0, sizeof(int) * (size_t)(g.n_cells + 1), st);
   if (e != cudaSuccess) return -1000 - (int)e;
-  gather_kernel<<<nb, T, 0, st>>>(g.n_sites, vals_b, p3, t, bx, by, bz, bt, bidx, f4);
-  cell_start_kernel<<<(unsigned)((g.n_cells + 1 + T - 1) / T), T, 0, st>>>(g.n_sites, g.n_cells,
-                                                                          keys_b, cell_start, ctr);
-  return 3 + 2 * ((key_bits(g.n_cells) + 7) / 8);  // ours + CUB's onesweep passes (approx.)
+  keys_kernel<<<nb, T, 0, st>>>(g, p3, t, dropped, keys_a, vals_a, cell_start, prm);
+  size_t bytes = cub_tmp_bytes;
+  // stable: equal cells keep ascending site order, as before
+  e = cub::DeviceRadixSort::SortPairs(cub_tmp, bytes, keys_a, keys_b, vals_a, vals_b,
+                                                  (int)g.n_sites, 0, key_bits(g.n_cells), st);
+  if (e != cudaSuccess) return -1000 - (int)e;
+  bytes = cub_tmp_bytes;
+  e = cub::DeviceScan::ExclusiveSum(cub_tmp, bytes, cell_start, cell_start, (int)(g.n_cells + 1), st);
+  if (e != cudaSuccess) return -1000 - (int)e;
+  gather_kernel<<<nb, T, 0, st>>>(g.n_sites, vals_b, p3, t, bx, by, bz, bt, bidx, f4, cell_start, g.n_cells,
+                                  ctr);
+  return 4 + 2 * ((key_bits(g.n_cells) + 7) / 8);  // ours + CUB's onesweep and scan passes (approx.)
 }
 
 }  // namespace vxb

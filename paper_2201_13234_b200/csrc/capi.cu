@@ -689,7 +689,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       unsigned* kb = ensure<unsigned>(ctx->keys_b, (size_t)ns);
       int* va = ensure<int>(ctx->vals_a, (size_t)ns);
       int* vb = ensure<int>(ctx->vals_b, (size_t)ns);
-      const size_t cub_bytes = bin_tmp_bytes(ns);
+      const size_t cub_bytes = bin_tmp_bytes(ns, g.n_cells);
       void* cub = ensure<char>(ctx->cub, cub_bytes);
       double* scratch = ensure<double>(ctx->scratch, 1024);
       const long long cap = (long long)std::min<int64_t>(nvs, 1ll << 22);
@@ -1133,7 +1133,7 @@ int vx_prune(vx_context* ctx_in, const vx_problem* P, uint8_t* dropped_out, int6
       unsigned* kb = ensure<unsigned>(ctx->keys_b, (size_t)ns);
       int* va = ensure<int>(ctx->vals_a, (size_t)ns);
       int* vb = ensure<int>(ctx->vals_b, (size_t)ns);
-      const size_t cub_bytes = bin_tmp_bytes(ns);
+      const size_t cub_bytes = bin_tmp_bytes(ns, g.n_cells);
       void* cub = ensure<char>(ctx->cub, cub_bytes);
       bins.x = bx; bins.y = by; bins.z = bz; bins.t = bt; bins.idx = bidx; bins.cell_start = cs;
       bins.f4 = nullptr;
