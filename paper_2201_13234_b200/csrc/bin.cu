@@ -33,7 +33,7 @@ __global__ void ingest_kernel(Geo g, Len16 len, int dim_in, const double* __rest
 #pragma unroll
     for (int a = 0; a < 3; ++a) p3[3 * s + a] = q[a];
   }
-  if (g.kind != kVoronoi) {
+  if (g.kind != kVoronoi && t_out) {
     double t;
     if (times_in) t = times_in[s];
     else t = __ddiv_rn(-weights_in[s], g.growth);

@@ -645,13 +645,19 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
     g.vec_store = (g.n[0] % 4 == 0) && ((reinterpret_cast<uintptr_t>(lab) & 15) == 0);
     DevParams* prm = ensure<DevParams>(ctx->params, 1);
     DevCounters* ctr = ensure<DevCounters>(ctx->counters, 1);
-    double* tdev = timed(P) ? ensure<double>(ctx->t, (size_t)ns) : nullptr;
-    double* p3 = use_brute ? nullptr : ensure<double>(ctx->p3, (size_t)ns * 3);
+    // 3-D positions already are the internal xyz AoS, and given birth times
+    // the time array: the ingest kernel then only validates (no copies)
+    const bool p3_alias = !use_brute && d == 3 && g.emb[0] == 0 && g.emb[1] == 1 && g.emb[2] == 2;
+    const bool t_alias = timed(P) && times != nullptr;
+    double* t_copy = timed(P) && !t_alias ? ensure<double>(ctx->t, (size_t)ns) : nullptr;
+    double* p3_copy = use_brute || p3_alias ? nullptr : ensure<double>(ctx->p3, (size_t)ns * 3);
+    const double* tdev = t_alias ? times : t_copy;
+    const double* p3 = p3_alias ? pos : p3_copy;
     Len16 len;
     for (int i = 0; i < 16; ++i) len.L[i] = i < d ? P->lengths[i] : 1.0;
     trace.rec(4, st);
     launches += launch_init(prm, ctr, st);
-    launches += launch_ingest(g, len, d, pos, times, weights, p3, tdev, ctr, st);
+    launches += launch_ingest(g, len, d, pos, times, weights, p3_copy, t_copy, ctr, st);
     dbg(st, "ingest");
     if (host_io) {  // fail before any labelling work (SiteSet::validate)
       ck(cudaMemcpyAsync(&ctx->h_ctr->bad_site, &ctr->bad_site, sizeof(unsigned), cudaMemcpyDeviceToHost, st),
