@@ -247,7 +247,7 @@ double host_time(const vx_problem* P, int64_t s) {
   return P->times ? P->times[s] : -(P->weights[s]) / P->growth;
 }
 
-void fill_geo(Geo& g, const vx_problem* P, int64_t zb, int64_t ze, int64_t n_for_cells) {
+void fill_geo(Geo& g, const vx_problem* P, int64_t zb, int64_t ze, int64_t n_for_cells, bool xy2d = false) {
   std::memset(&g, 0, sizeof(g));
   g.kind = P->kind;
   g.periodic = P->periodic ? 1 : 0;
@@ -259,10 +259,14 @@ void fill_geo(Geo& g, const vx_problem* P, int64_t zb, int64_t ze, int64_t n_for
   g.lmax = 0.0;
   // true axis a -> embedded axis; the last true axis is always z (see Geo)
   static const int kEmb[4][3] = {{0, 1, 2}, {2, 0, 0}, {0, 2, 0}, {0, 1, 2}};
+  // xy2d: a whole 2-D image maps to embedded (x, y) with a one-voxel z, so an
+  // 8 x 8 x 4 sub-brick holds 64 voxels instead of 32 (the slab axis z is then
+  // the padded one: callers pass zb = 0, ze = 1)
+  static const int kEmb2xy[3] = {0, 1, 2};
   const int dd = P->dim <= 3 ? P->dim : 3;
   bool real[3] = {false, false, false};
   for (int a = 0; a < 3; ++a) {
-    g.emb[a] = kEmb[dd][a];
+    g.emb[a] = xy2d ? kEmb2xy[a] : kEmb[dd][a];
     g.n[a] = 1;
     g.L[a] = 1.0;
   }
@@ -481,7 +485,8 @@ int write_sink(vx_context* ctx, const vx_problem* P, const FileSink& sink, const
       if (!rc) rc = rc2;
     }
   if (rc || sink.to_memory()) return rc;
-  const int64_t nv_total = plane * (P->counts[P->dim - 1]);
+  int64_t nv_total = 1;  // the files hold the whole image
+  for (int a = 0; a < P->dim; ++a) nv_total *= P->counts[a];
   rc = vx_write_image_sidecar(sink.lab_path, "labels", P->dim, P->counts, P->lengths, P->periodic, P->kind,
                               P->n_sites, sink.seed, (uint64_t)nv_total * 4u);
   if (!rc && dist)
@@ -546,6 +551,10 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
   if (zb == 0 && ze == 0) ze = n_last;
   if (!(zb >= 0 && zb < ze && ze <= n_last))
     return fail(VX_EINVAL, "slab must satisfy 0 <= slab_begin < slab_end <= counts[dim-1]");
+  // a whole 2-D image: (x, y) embedding, one "plane" of n0 n1 voxels
+  // (embedded y rides in gridDim.y of the ball kernels: <= 65535 super-brick rows)
+  const bool xy2d = d == 2 && !brute_engine && zb == 0 && ze == n_last && n_last <= 1000000 &&
+                    !std::getenv("VX_2D_XZ");
   if (O.asynchronous && !O.device_pointers)
     return fail(VX_EINVAL, "asynchronous calls need device pointers");
   const bool host_io = !O.device_pointers;
@@ -588,6 +597,11 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
   int launches = 0;
   int64_t plane = 1;
   for (int i = 0; i < d - 1; ++i) plane *= P->counts[i];
+  if (xy2d) {
+    plane *= n_last;
+    zb = 0;
+    ze = 1;
+  }
   const int64_t nvs = plane * (ze - zb);
   const int64_t ns = P->n_sites;
   StageTimer tm;
@@ -624,7 +638,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       }
     }
     Geo g;
-    fill_geo(g, P, zb, ze, ns);
+    fill_geo(g, P, zb, ze, ns, xy2d);
     int32_t* lab = host_io ? ensure<int32_t>(ctx->labels, (size_t)nvs) : labels_out;
     double* dist = nullptr;
     // host-buffer call into pageable memory: stage through pinned buffers
