@@ -552,9 +552,10 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
   if (!(zb >= 0 && zb < ze && ze <= n_last))
     return fail(VX_EINVAL, "slab must satisfy 0 <= slab_begin < slab_end <= counts[dim-1]");
   // a whole 2-D image: (x, y) embedding, one "plane" of n0 n1 voxels
-  // (embedded y rides in gridDim.y of the ball kernels: <= 65535 super-brick rows)
-  const bool xy2d = d == 2 && !brute_engine && zb == 0 && ze == n_last && n_last <= 1000000 &&
-                    !std::getenv("VX_2D_XZ");
+  // (embedded y rides in gridDim.y of the ball kernels: <= 65535 super-brick
+  // rows); a whole 1-D image likewise maps to embedded x
+  const bool xy2d = (d == 2 || d == 1) && !brute_engine && zb == 0 && ze == n_last &&
+                    (d == 1 || n_last <= 1000000) && !std::getenv("VX_2D_XZ");
   if (O.asynchronous && !O.device_pointers)
     return fail(VX_EINVAL, "asynchronous calls need device pointers");
   const bool host_io = !O.device_pointers;
