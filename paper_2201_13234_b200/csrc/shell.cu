@@ -24,6 +24,8 @@ __device__ __forceinline__ long long wrapm(long long c, long long m) {
   const long long r = c % m;
   return r < 0 ? r + m : r;
 }
+// c in (-m, 2m): the periodic cell index in [0, m)
+__device__ __forceinline__ int wrap1(int c, int m) { return c < 0 ? c + m : (c >= m ? c - m : c); }
 
 template <int KIND, bool PER>
 __device__ void shell_one(const Geo& g, const Bins& bins, const DevParams* prm, long long lin,
@@ -69,20 +71,22 @@ __device__ void shell_one(const Geo& g, const Bins& bins, const DevParams* prm, 
       }
       allfull &= full[a];
     }
-    const long long sx = hi[0] - lo[0] + 1, sy = hi[1] - lo[1] + 1, sz = hi[2] - lo[2] + 1;
-    const long long ncell = sx * sy * sz;
-    for (long long f = lane; f < ncell; f += 32) {
-      const long long ix = lo[0] + f % sx, iy = lo[1] + (f / sx) % sy, iz = lo[2] + f / (sx * sy);
-      const long long w[3] = {PER ? wrapm(ix, g.m[0]) : ix, PER ? wrapm(iy, g.m[1]) : iy,
-                              PER ? wrapm(iz, g.m[2]) : iz};
+    // 32-bit cell arithmetic: m <= 4096 per axis, windows never exceed the
+    // grid (n_cells <= 2^26), and |index| < 2m so one conditional wraps it
+    const int sx = (int)(hi[0] - lo[0] + 1), sy = (int)(hi[1] - lo[1] + 1), sz = (int)(hi[2] - lo[2] + 1);
+    const int ncell = sx * sy * sz;
+    for (int f = lane; f < ncell; f += 32) {
+      const int fyz = f / sx;
+      const int ix = (int)lo[0] + (f - fyz * sx), iy = (int)lo[1] + fyz % sy, iz = (int)lo[2] + fyz / sy;
+      const int w[3] = {PER ? wrap1(ix, g.m[0]) : ix, PER ? wrap1(iy, g.m[1]) : iy, PER ? wrap1(iz, g.m[2]) : iz};
       if (r > 0) {  // skip cells of the previous window
         bool inside = true;
-        const long long u[3] = {ix, iy, iz};
+        const int u[3] = {ix, iy, iz};
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
           bool in_a;
           if (pfull[a]) in_a = true;
-          else if (PER) in_a = wrapm(w[a] - plo[a], g.m[a]) <= phi[a] - plo[a];
+          else if (PER) in_a = wrap1(w[a] - (int)plo[a], g.m[a]) <= (int)(phi[a] - plo[a]);
           else in_a = u[a] >= plo[a] && u[a] <= phi[a];
           inside &= in_a;
         }
