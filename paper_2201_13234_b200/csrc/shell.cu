@@ -27,6 +27,52 @@ __device__ __forceinline__ long long wrapm(long long c, long long m) {
 // c in (-m, 2m): the periodic cell index in [0, m)
 __device__ __forceinline__ int wrap1(int c, int m) { return c < 0 ? c + m : (c >= m ? c - m : c); }
 
+// Few sites (n_alive <= kShellBrute): every alive site, 32 lanes at a time, is
+// cheaper than the ring bookkeeping; the same exact (prox, index) minimum.
+constexpr int kShellBrute = 2048;
+
+template <int KIND, bool PER>
+__device__ void shell_all(const Geo& g, const Bins& bins, int n_alive, long long lin, int* labels,
+                          double* dist, unsigned long long* hist, unsigned long long* evals) {
+  const int lane = threadIdx.x & 31;
+  const long long kx = lin % g.n[0];
+  const long long ky = (lin / g.n[0]) % g.n[1];
+  const long long kz = lin / (g.n[0] * g.n[1]);
+  const double c[3] = {center(kx, g.sp[0]), center(ky, g.sp[1]), center(kz, g.sp[2])};
+  const bool g1 = g.g_is_one;
+  double best = __longlong_as_double(0x7ff0000000000000ll);
+  int bi = 0x7fffffff;
+  for (int p = lane; p < n_alive; p += 32) {
+    // reference fold: s = 0; s += w_z^2; s += w_y^2; s += w_x^2
+    const double az = axis_sq<PER>(bins.z[p], c[2], g.L[2], g.invL[2]);
+    const double ay = axis_sq<PER>(bins.y[p], c[1], g.L[1], g.invL[1]);
+    const double ax = axis_sq<PER>(bins.x[p], c[0], g.L[0], g.invL[0]);
+    const double dsq = __dadd_rn(__dadd_rn(az, ay), ax);
+    const double pr = prox_from_dsq<KIND>(dsq, g.growth, g1, KIND == kVoronoi ? 0.0 : bins.t[p]);
+    const int id = bins.idx[p];
+    if (pr < best || (pr == best && id < bi)) {
+      best = pr;
+      bi = id;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob < best || (ob == best && oi < bi)) {
+      best = ob;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    const long long out = lin - g.z_begin * g.n[0] * g.n[1];
+    labels[out] = bi;
+    if (dist) dist[out] = KIND == kVoronoi ? __dsqrt_rn(best) : best;
+    if (hist) atomicAdd(&hist[bi], 1ull);
+    *evals += (unsigned long long)n_alive;
+  }
+}
+
 template <int KIND, bool PER>
 __device__ void shell_one(const Geo& g, const Bins& bins, const DevParams* prm, long long lin,
                           int* labels, double* dist, unsigned long long* hist,
@@ -165,12 +211,14 @@ __global__ void __launch_bounds__(kShellThreads)
   const long long nwarps = (long long)gridDim.x * (kShellThreads / 32);
   const long long w = blockIdx.x * (long long)(kShellThreads / 32) + (threadIdx.x >> 5);
   const long long n = (long long)ctr->n_unres;
+  const int n_alive = (int)ctr->n_alive;  // binned (prune-surviving) sites
   unsigned long long ne = 0;
   if (n <= unres_cap) {
     for (long long i = w; i < n; i += nwarps) {
       VXCHK(unres[i] >= 0 && unres[i] < g.n[0] * g.n[1] * g.n[2], "unres[%lld]=%lld n=%lld", i,
             unres[i], n);
-      shell_one<KIND, PER>(g, bins, prm, unres[i], labels, dist, hist, &ne);
+      if (n_alive <= kShellBrute) shell_all<KIND, PER>(g, bins, n_alive, unres[i], labels, dist, hist, &ne);
+      else shell_one<KIND, PER>(g, bins, prm, unres[i], labels, dist, hist, &ne);
     }
   } else {
     // overflow: compact directly from the image (label sentinel -1)
@@ -184,7 +232,8 @@ __global__ void __launch_bounds__(kShellThreads)
       while (mask) {
         const int src = __ffs(mask) - 1;
         mask &= mask - 1;
-        shell_one<KIND, PER>(g, bins, prm, base + c0 + src, labels, dist, hist, &ne);
+        if (n_alive <= kShellBrute) shell_all<KIND, PER>(g, bins, n_alive, base + c0 + src, labels, dist, hist, &ne);
+        else shell_one<KIND, PER>(g, bins, prm, base + c0 + src, labels, dist, hist, &ne);
       }
     }
   }
