@@ -924,3 +924,48 @@ def test_polydisperse_laguerre_spheres(oracle_mod, periodic, sigma, growth):
         assert np.array_equal(bits(r.distances.values), bits(dist))
     if sigma > 0.5:
         assert dropped.any()  # the pruning path is exercised
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", ["z_sorted", "x_sorted", "morton", "blocks"])
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_site_index_order_vs_reference(order, kind):
+    """The cull's per-super-brick index sort buckets the kept sites by site
+    index and falls back to the all-pairs rank when the indices crowd into
+    few buckets -- e.g. sites numbered in spatial order.  Both routes against
+    the reference library, bit for bit."""
+    import oracle
+    import paper_2201_13234_b200 as vx
+
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    counts, ns = [160, 144, 176], 6000
+    L = np.array([1.0, 0.9, 1.1])
+    pos, t = oracle.generate_uniform_sites(3, L, ns, kind, 0.5 * np.cbrt(np.prod(L) / ns), 71 + kind)
+    P = pos.reshape(ns, 3)
+    if order == "z_sorted":
+        perm = np.argsort(P[:, 2], kind="stable")
+    elif order == "x_sorted":
+        perm = np.lexsort((P[:, 1], P[:, 0]))
+    elif order == "morton":  # Z-order curve: every neighbourhood is a few dense index runs
+        q = np.minimum((P / L * 1024).astype(np.uint64), np.uint64(1023))
+        key = np.zeros(ns, dtype=np.uint64)
+        for b in range(10):
+            for a in range(3):
+                key |= ((q[:, a] >> np.uint64(b)) & np.uint64(1)) << np.uint64(3 * b + a)
+        perm = np.argsort(key, kind="stable")
+    else:  # spatial blocks of 8^3 cells, shuffled block order
+        cell = np.floor(P / (L / 8)).astype(np.int64)
+        key = cell[:, 0] + 8 * (cell[:, 1] + 8 * cell[:, 2])
+        rank = np.random.default_rng(5).permutation(512)
+        perm = np.argsort(rank[key], kind="stable")
+    pos = np.ascontiguousarray(P[perm]).reshape(-1)
+    t = None if t is None else np.ascontiguousarray(t[perm])
+    for periodic in (True, False):
+        p = oracle.Problem(kind, counts, L, periodic, pos, t, 0.0 if kind == 0 else 1.1)
+        lab_ref, dist_ref, _, _ = oracle.ref_tessellate(p)
+        sites, grid = to_vx(p)
+        r = vx.tessellate_fast(sites, grid, distances=True, histogram=True)
+        assert np.array_equal(r.labels.labels, lab_ref), int((r.labels.labels != lab_ref).sum())
+        assert np.array_equal(r.distances.values.view(np.uint64), dist_ref.view(np.uint64))
+        assert np.array_equal(r.histogram, np.bincount(lab_ref, minlength=ns).astype(np.uint64))
