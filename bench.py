@@ -161,6 +161,12 @@ def run_reference(args):
     c, box, grid, sites = make_inputs(args.config)
     threads = os.cpu_count() or 1
     planes = args.ref_planes
+    # keep the whole arm within ~--ref-budget-s: at 320 planes a cfg5 sample
+    # takes ~5.2 s on the box's 16 cores, so long --steps runs sample fewer
+    # planes (smaller samples slightly under-state the reference's rate)
+    if c["n"] == 1000 and args.ref_budget_s > 0:
+        fit = int(320 * args.ref_budget_s / (5.2 * (args.warmup + args.steps)))
+        planes = max(32, min(planes, fit))
     try:
         times = []
         for i in range(args.warmup + args.steps):
@@ -387,6 +393,7 @@ def main():
     ap.add_argument("--cpu-planes", type=int, default=320)  # ~10 s of reference CPU work at cfg5
     # 320 planes: the sampled rate matches a full reference run on the box (fixed per-call costs amortised)
     ap.add_argument("--ref-planes", type=int, default=320)
+    ap.add_argument("--ref-budget-s", type=float, default=200.0)
     # functional dry run of the N > 1 path on a one-GPU box (not a measurement):
     # gloo collectives, every rank on cuda:0
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"], help=argparse.SUPPRESS)
