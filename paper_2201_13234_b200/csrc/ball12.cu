@@ -765,18 +765,24 @@ __device__ __forceinline__ void exact_tables(ES& ws, const Bins& bins, const Geo
   }
 }
 
-constexpr int kEvalWarps = 2;  // sub-bricks along y per CTA
+// one sub-brick (warp) per CTA: a CTA slot frees as soon as its sub-brick is
+// done (1 / 2 / 4 warps per CTA: cfg5 eval+cull 6.79 / 6.92 / 6.97 ms)
+#ifndef VX_EVAL_WARPS
+#define VX_EVAL_WARPS 1
+#endif
+constexpr int kEvalWarps = VX_EVAL_WARPS;  // sub-bricks along y per CTA
+constexpr unsigned kMaxGridY = 65535;      // gridDim.y limit: taller grids launch in y-chunks
 
 // One warp per 8x8x4 sub-brick (the tail of v11's sub-brick loop: exact
 // tables, evaluation, stores, histogram, unresolved compaction).  The site
 // index load is issued before the tables and consumed at the store.
 template <int KIND, bool PER, bool DENSE, bool FA>
-__global__ void __launch_bounds__(kEvalWarps * 32, 16)
+__global__ void __launch_bounds__(kEvalWarps * 32, 32 / kEvalWarps)
     eval12_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, const int2* __restrict__ info,
                   const int* __restrict__ slots16, const int* __restrict__ list, int* __restrict__ labels,
                   double* __restrict__ dist,
                   unsigned long long* __restrict__ hist, long long* __restrict__ unres, long long unres_cap,
-                  DevCounters* ctr, unsigned long long* __restrict__ eval_slots, long long nsb) {
+                  DevCounters* ctr, unsigned long long* __restrict__ eval_slots, long long nsb, unsigned sby0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   using ES = EvalSmemT<DENSE ? kLcapD : kFcap>;
@@ -785,7 +791,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 16)
   const double cutoff = prm->cutoff;
   const int qx = (lane & 1) * 4, vy = (lane >> 1) & 3, vz = lane >> 3;
   // grid (nsbx, ceil(nsby / 8), nsbz): no index division
-  const unsigned sbx = blockIdx.x, sby = blockIdx.y * kEvalWarps + wid, sbz = blockIdx.z;
+  const unsigned sbx = blockIdx.x, sby = sby0 + blockIdx.y * kEvalWarps + wid, sbz = blockIdx.z;
   if (sby >= nsby) return;
   const long long sb = (long long)sbx + (long long)nsbx * ((long long)sby + (long long)nsby * sbz);
   const int2 inf = info[sb];
@@ -1035,7 +1041,7 @@ bool ball12_dense(const Geo& g) {
 }
 
 template <int KIND, bool PER, bool DENSE>
-static void launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* labels, double* dist,
+static int launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* labels, double* dist,
                      unsigned long long* hist, long long* unres, long long cap, DevCounters* ctr,
                      unsigned long long* slots, int2* info, int* slots16, int* list, long long list_cap,
                      int* list_count, int* ovf, int nbb, cudaStream_t st) {
@@ -1060,15 +1066,21 @@ static void launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* 
   v12::cull12_kernel<KIND, PER, DENSE><<<grid, v12::kB2Threads, sh_c, st>>>(g, bins, prm, info, slots16, list, list_cap,
                                                                      list_count, ovf, ctr, slots, nbb);
   const long long nsb = ball12_subbricks(g);
-  const dim3 eg((unsigned)((g.n[0] + 7) / 8), (unsigned)(((g.n[1] + 7) / 8 + v12::kEvalWarps - 1) / v12::kEvalWarps),
-                (unsigned)((g.z_end - g.z_begin + 3) / 4));
-  if (KIND != kVoronoi && g.fast_arith)  // call-free exact sqrt / division (vx_internal.cuh)
-    v12::eval12_kernel<KIND, PER, DENSE, KIND != kVoronoi><<<eg, v12::kEvalWarps * 32, sh_e, st>>>(
-        g, bins, prm, info, slots16, list, labels, dist, hist, unres, cap, ctr, slots, nsb);
-  else
-    v12::eval12_kernel<KIND, PER, DENSE, false><<<eg, v12::kEvalWarps * 32, sh_e, st>>>(
-        g, bins, prm, info, slots16, list, labels, dist, hist, unres, cap, ctr, slots, nsb);
+  const long long rows = ((g.n[1] + 7) / 8 + v12::kEvalWarps - 1) / v12::kEvalWarps;  // CTA rows along y
+  int launches = 0;
+  for (long long r0 = 0; r0 < rows; r0 += v12::kMaxGridY, ++launches) {
+    const dim3 eg((unsigned)((g.n[0] + 7) / 8), (unsigned)std::min<long long>(v12::kMaxGridY, rows - r0),
+                  (unsigned)((g.z_end - g.z_begin + 3) / 4));
+    const unsigned sby0 = (unsigned)(r0 * v12::kEvalWarps);
+    if (KIND != kVoronoi && g.fast_arith)  // call-free exact sqrt / division (vx_internal.cuh)
+      v12::eval12_kernel<KIND, PER, DENSE, KIND != kVoronoi><<<eg, v12::kEvalWarps * 32, sh_e, st>>>(
+          g, bins, prm, info, slots16, list, labels, dist, hist, unres, cap, ctr, slots, nsb, sby0);
+    else
+      v12::eval12_kernel<KIND, PER, DENSE, false><<<eg, v12::kEvalWarps * 32, sh_e, st>>>(
+          g, bins, prm, info, slots16, list, labels, dist, hist, unres, cap, ctr, slots, nsb, sby0);
+  }
   launch_subshell(g, bins, prm, ovf, &ctr->n_ovf_sb, labels, dist, hist, ctr, st);
+  return launches - 1;  // eval launches beyond the first
 }
 
 int launch_ball12(const Geo& g, const Bins& bins, const DevParams* prm, int* labels, double* dist,
@@ -1082,8 +1094,9 @@ int launch_ball12(const Geo& g, const Bins& bins, const DevParams* prm, int* lab
   static const int nbb_env = std::getenv("VX_NBB") ? std::atoi(std::getenv("VX_NBB")) : 0;
   const int nbb = nbb_env == 1 || nbb_env == 2 || nbb_env == 4 ? nbb_env : choose_nbb12(g);
   const bool dense = ball12_dense(g);
+  int extra = 0;
 #define VX_L12(K, P)                                                                                          \
-  (dense ? launch12<K, P, true>(g, bins, prm, labels, dist, hist, unres, unres_cap, ctr, slots, info, slots16, \
+  extra = (dense ? launch12<K, P, true>(g, bins, prm, labels, dist, hist, unres, unres_cap, ctr, slots, info, slots16, \
                                 list, list_cap, list_count, ovf, nbb, st)                                     \
          : launch12<K, P, false>(g, bins, prm, labels, dist, hist, unres, unres_cap, ctr, slots, info, slots16, \
                                  list, list_cap, list_count, ovf, nbb, st))
@@ -1097,7 +1110,7 @@ int launch_ball12(const Geo& g, const Bins& bins, const DevParams* prm, int* lab
   }
 #undef VX_L12
   ball12_publish_kernel<<<1, 32, 0, st>>>(slots, ctr);
-  return 4;
+  return 4 + extra;
 }
 
 }  // namespace vxb

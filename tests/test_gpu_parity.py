@@ -530,10 +530,12 @@ def test_dense_mode_vs_reference(kind, per):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("d,counts,ns", [(1, [600000], 3000), (2, [4, 300000], 2000)])
+@pytest.mark.parametrize("d,counts,ns", [(1, [600000], 3000), (2, [4, 300000], 2000), (2, [3, 700000], 4000),
+                                         (3, [2, 600000, 2], 3000)])
 def test_long_last_axis_vs_reference(d, counts, ns):
     """Last axes longer than one launch's grid (262,080 planes) are labelled in
-    several z-chunks; bit-exact against the reference library."""
+    several z-chunks, and embedded y axes longer than 65,535 sub-bricks in
+    several eval launches; bit-exact against the reference library."""
     import oracle
     import paper_2201_13234_b200 as vx
 
