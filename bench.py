@@ -13,10 +13,12 @@ the launching stream; L2 is flushed between steps (outside the events).
 
 ``e2e`` is the same metric through the public API with host buffers: H2D of the
 sites from pinned memory and D2H of the whole label image + histogram inside
-the timed region.  ``cpu_baseline`` times the reference library (oracle/_ref,
-compiled from the reference's own sources) on this host's cores on a bounded
-z-slab sample of the same workload.  ``--impl reference`` prints the same line
-for the reference CPU implementation alone.
+the timed region.  ``cpu_baseline`` times one stock ``tessellate_fast`` call of
+the reference library (oracle/_ref, compiled from the reference's own sources)
+on this host's cores over the whole config, and compares its label image with
+ours.  ``--impl reference`` prints the same line for the reference CPU
+implementation alone: each step one stock ``tessellate_fast`` of the whole
+config, inputs from the reference's own generator, the product never loaded.
 """
 from __future__ import annotations
 
@@ -44,6 +46,8 @@ CONFIGS = {
     1: dict(name="cfg1: 3D periodic Voronoi 128^3, Ns=1000", kind=0, n=128, ns=1000, periodic=True),
     2: dict(name="cfg2: 3D non-periodic Voronoi 512^3, Ns=1e5", kind=0, n=512, ns=100000,
             periodic=False),
+    3: dict(name="cfg3: 3D periodic Laguerre 512^3, Ns=5e4, w=r^2, r lognormal (sigma=0.3, mean 0.5 Ns^-1/3)",
+            kind=2, n=512, ns=50000, periodic=True),
     4: dict(name="cfg4: 3D periodic Johnson-Mehl 512^3, Ns=2e4, t~U[0,0.5 Ns^-1/3), v=1", kind=1,
             n=512, ns=20000, periodic=True),
     5: dict(name="cfg5: 3D periodic Voronoi 1000^3 (1e9 voxels), Ns=1e6", kind=0, n=1000,
@@ -62,16 +66,120 @@ def dist_env():
     return world, rank, local
 
 
+class MT64:
+    """std::mt19937_64 ([rand.eng.mers]; the sequence is fixed by the C++
+    standard), in plain Python so that both arms draw the cfg3 spheres from the
+    same code without importing either library."""
+
+    def __init__(self, seed):
+        M = (1 << 64) - 1
+        mt = [seed & M]
+        for i in range(1, 312):
+            mt.append((6364136223846793005 * (mt[-1] ^ (mt[-1] >> 62)) + i) & M)
+        self.mt, self.i = mt, 312
+
+    def _twist(self):
+        mt = self.mt
+        for i in range(312):
+            x = (mt[i] & 0xFFFFFFFF80000000) | (mt[(i + 1) % 312] & 0x7FFFFFFF)
+            y = x >> 1
+            if x & 1:
+                y ^= 0xB5026F5AA96619E9
+            mt[i] = mt[(i + 156) % 312] ^ y
+        self.i = 0
+
+    def next(self):
+        if self.i >= 312:
+            self._twist()
+        x = self.mt[self.i]
+        self.i += 1
+        x ^= (x >> 29) & 0x5555555555555555
+        x ^= (x << 17) & 0x71D67FFFEDA60000
+        x ^= (x << 37) & 0xFFF7EEE000000000
+        x &= (1 << 64) - 1
+        return x ^ (x >> 43)
+
+    def u01(self):  # uniform01, sites.cpp:20-22
+        return float(self.next() >> 11) * 2.0 ** -53
+
+
+def lognormal_spheres(n, seed, sigma=0.3):
+    """SURVEY.md App. C cfg3 recipe: per sphere x, y, z = u01 (0 redrawn),
+    a = u01 (0 redrawn), b = u01, z = sqrt(-2 ln a) cos(2 pi b),
+    r = m exp(sigma z - sigma^2 / 2), m = 0.5 cbrt(1 / n) (glibc libm through
+    the math module, as the C restatement oracle/vx_oracle.c uses)."""
+    g = MT64(seed)
+    m = 0.5 * float(np.cbrt(1.0 / n))  # as oracle.baseline_config(3)
+    pos = np.empty(3 * n)
+    rad = np.empty(n)
+    two_pi = 2.0 * 3.14159265358979323846
+    for s in range(n):
+        for i in range(3):
+            u = g.u01()
+            while u == 0.0:
+                u = g.u01()
+            pos[3 * s + i] = u
+        a = g.u01()
+        while a == 0.0:
+            a = g.u01()
+        b = g.u01()
+        z = math.sqrt(-2.0 * math.log(a)) * math.cos(two_pi * b)
+        rad[s] = m * math.exp(sigma * z - 0.5 * sigma * sigma)
+    return pos, rad
+
+
+def horizon_of(c):
+    return 0.5 * math.pow(1.0 / c["ns"], 1.0 / 3.0)
+
+
 def make_inputs(cfg_id):
+    """Our arm: SURVEY.md App. C inputs through the product's own API."""
     import paper_2201_13234_b200 as vx
 
     c = CONFIGS[cfg_id]
     box = vx.Domain([1.0, 1.0, 1.0], vx.Boundary.Periodic if c["periodic"] else vx.Boundary.NonPeriodic)
     grid = vx.VoxelGrid([c["n"]] * 3, box)
-    horizon = 0.5 * math.pow(1.0 / c["ns"], 1.0 / 3.0)
-    sites = vx.generate_uniform_sites(box, c["ns"], vx.Kind(c["kind"]), 1.0 if c["kind"] else 0.0,
-                                      horizon, 1000 + cfg_id)
+    if c["kind"] == 2:
+        pos, rad = lognormal_spheres(c["ns"], 1000 + cfg_id)
+        sites = vx.spheres_to_timed_sites(vx.LaguerreSpheres(3, pos, rad), 1.0)
+    else:
+        sites = vx.generate_uniform_sites(box, c["ns"], vx.Kind(c["kind"]), 1.0 if c["kind"] else 0.0,
+                                          horizon_of(c), 1000 + cfg_id)
     return c, box, grid, sites
+
+
+def make_ref_problem(cfg_id):
+    """Reference arm: the same inputs through the reference library's own
+    generator (sites.cpp:61-104); never imports the product."""
+    import oracle  # the --impl reference / cpu_baseline leg only
+
+    c = CONFIGS[cfg_id]
+    one = np.ones(3)
+    if c["kind"] == 2:
+        pos, rad = lognormal_spheres(c["ns"], 1000 + cfg_id)
+        t = oracle.ref_spheres_to_timed(pos, rad, 1.0)
+        return oracle.Problem(2, [c["n"]] * 3, one, c["periodic"], pos, t, 1.0)
+    pos, t = oracle.ref_generate_uniform_sites(3, one, c["ns"], c["kind"], 1.0 if c["kind"] else 0.0,
+                                               horizon_of(c), 1000 + cfg_id)
+    return oracle.Problem(c["kind"], [c["n"]] * 3, one, c["periodic"], pos, t, 1.0 if c["kind"] else 0.0)
+
+
+def config_dict(c, world):
+    """The workload description, identical in both arms."""
+    return {"workload": c["name"], "n_voxels": c["n"] ** 3, "n_sites": c["ns"],
+            "kind": ["voronoi", "johnson-mehl", "laguerre"][c["kind"]], "periodic": c["periodic"],
+            "inputs": "SURVEY.md App. C seeded sites (mt19937_64, seed 1000+cfg)",
+            "labels": "int32 (reference u32), bit-exact", "histogram": "grain volumes",
+            "parallelism": f"z-slab x{world}",
+            "l2": "flushed between steps (256 MB write); labels 4 B/voxel > L2"}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
 
 
 class ClockSampler:
@@ -140,57 +248,57 @@ def load_traffic(cfg_id):
         return None
 
 
-def cpu_reference_sample(c, sites, planes, threads):
-    """The reference's own CPU engine (oracle/_ref) on z-slab [0, planes)."""
-    import oracle  # bench's cpu_baseline / --impl reference leg only
-
-    if not oracle.have_ref():
-        raise FileNotFoundError("oracle/_ref/libvoxellate_ref.so not built")
-    p = oracle.Problem(c["kind"], [c["n"]] * 3, np.ones(3), c["periodic"], sites.positions,
-                       sites.times, sites.growth)
-    t0 = time.perf_counter()
-    lab, _ = oracle.ref_slab_sample(p, 0, planes, threads=threads)
-    dt = time.perf_counter() - t0
-    return dt, lab
+def ref_threads():
+    return os.cpu_count() or 1
 
 
 def run_reference(args):
+    """The reference's own CPU implementation (oracle/_ref: the library compiled
+    from /root/reference's sources): each step one stock tessellate_fast call
+    with default options on the WHOLE config, all host threads."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    c, box, grid, sites = make_inputs(args.config)
-    threads = os.cpu_count() or 1
-    planes = args.ref_planes
-    # keep the whole arm within ~--ref-budget-s: at 320 planes a cfg5 sample
-    # takes ~5.2 s on the box's 16 cores, so long --steps runs sample fewer
-    # planes (smaller samples slightly under-state the reference's rate)
-    if c["n"] == 1000 and args.ref_budget_s > 0:
-        fit = int(320 * args.ref_budget_s / (5.2 * (args.warmup + args.steps)))
-        planes = max(32, min(planes, fit))
+    c = CONFIGS[args.config]
+    threads = ref_threads()
     try:
-        times = []
+        p = make_ref_problem(args.config)
+        times, fp, param = [], None, None
         for i in range(args.warmup + args.steps):
-            dt, _ = cpu_reference_sample(c, sites, planes, threads)
+            sec, f, param, _ = oracle_ref_tessellate(p, threads)
+            fp = fp or f
             if i >= args.warmup:
-                times.append(dt)
+                times.append(sec)
     except Exception as e:  # reference library missing on this box
         print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}))
         return 0
-    nv = planes * c["n"] * c["n"]
+    nv = c["n"] ** 3
     mean = float(np.mean(times))
     val = nv / mean / 1e9
-    sample = (f"z-slab [0,{planes}) of {c['n']}^3 = {nv} voxels, all {c['ns']} sites, "
-              f"reference step-1 window scan + step-2 full scan (oracle/_ref vxref_slab_sample)")
+    sample = (f"the whole config ({nv} voxels, {c['ns']} sites) per step: stock tessellate_fast "
+              f"(default FastOptions: prune on, model-optimal r0/t0) of the reference library "
+              f"(oracle/_ref), timed around the call, {threads} OpenMP threads")
     out = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (SURVEY.md App. C seeded sites)",
-           "config": {"workload": c["name"], "sample_planes": planes},
+           "data": "synthetic: SURVEY.md App. C seeded sites through the reference's own generator",
+           "config": config_dict(c, world),
            "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "reference",
                             "sample": sample},
-           "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "step_s": times, "param": param,
+           "parity": {"fingerprint": fp, "expected": EXPECTED_FP.get(args.config),
+                      "match": fp == EXPECTED_FP.get(args.config)}}
     print(json.dumps(out))
     return 0
+
+
+def oracle_ref_tessellate(p, threads, labels=False):
+    import oracle  # the --impl reference / cpu_baseline leg only
+
+    if not oracle.have_ref():
+        raise FileNotFoundError("oracle/_ref/libvoxellate_ref.so not built")
+    return oracle.ref_tessellate_timed(p, threads=threads, labels=labels)
 
 
 def run_ours(args):
@@ -284,6 +392,7 @@ def run_ours(args):
     # ---- e2e through the public API with host buffers ----
     e2e = None
     fp = None
+    out_h = None
     if not args.no_e2e:
         pin_pos = torch.from_numpy(sites.positions).pin_memory()
         sites_h = vx.SiteSet(sites.kind, 3, pin_pos.numpy(), None if sites.times is None else
@@ -308,6 +417,7 @@ def run_ours(args):
                "ms_per_step": float(t_e2e.item()) * 1e3, "host_buffers": "pinned"}
         if world == 1:
             fp = "%016x" % _lib.lib().vx_label_fingerprint(out.ctypes.data_as(_lib.C.c_void_p), out.size)
+            out_h = out
 
     if rank != 0:
         if dist is not None:
@@ -315,6 +425,10 @@ def run_ours(args):
         return 0
 
     # ---- roofline of the dominant kernel (ball) ----
+    hbm_peak = measured_peaks().get("hbm_gbs")
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs"
+    if not hbm_peak:
+        hbm_peak, hbm_src = 7672.0, "B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)"
     dadd = _lib.C.c_double(0.0)
     fadd = _lib.C.c_double(0.0)
     _lib.lib().vx_probe_pipe_rates(dev, _lib.C.byref(dadd), _lib.C.byref(fadd))
@@ -329,19 +443,24 @@ def run_ours(args):
                 "peak_source": "measured DADD issue rate (vx_probe_pipe_rates) on this GPU",
                 "hbm_view": {"label_bytes": 4 * nvs,
                              "achieved_gbs": 4 * nvs / (ball_ms * 1e-3) / 1e9,
-                             "peak_gbs": 6549.1, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
+                             "peak_gbs": hbm_peak, "peak_source": hbm_src}}
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
+        # one stock tessellate_fast of the reference library on the same
+        # inputs: the whole config (~16 s at cfg5 on 16 host threads)
+        threads = ref_threads()
         try:
-            dt, lab = cpu_reference_sample(c, sites, args.cpu_planes, threads)
-            nvc = args.cpu_planes * plane
-            same = bool(np.array_equal(lab.view(np.int32), labels_d[:nvc].cpu().numpy()))
-            cpu = {"value": nvc / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": f"z-slab [0,{args.cpu_planes}) of {n}^3 ({nvc} voxels, all {ns} sites), "
-                             f"reference engine via oracle/_ref, {dt:.2f} s wall",
-                   "labels_equal_gpu": same}
+            import oracle  # the cpu_baseline leg only (checker / baseline, never measured as ours)
+
+            p = oracle.Problem(c["kind"], [n] * 3, np.ones(3), c["periodic"], sites.positions, sites.times,
+                               sites.growth)
+            dt, rfp, _, lab = oracle_ref_tessellate(p, threads, labels=out_h is not None)
+            same = bool(np.array_equal(lab.view(np.int32), out_h)) if out_h is not None else None
+            cpu = {"value": nv_total / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"the whole config ({nv_total} voxels, {ns} sites): one stock tessellate_fast "
+                             f"(oracle/_ref, default FastOptions), {dt:.2f} s around the call",
+                   "labels_equal_gpu": same, "fingerprint": rfp}
         except Exception as e:
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {type(e).__name__}: {e}"}
@@ -352,13 +471,10 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: SURVEY.md App. C seeded uniform sites (mt19937_64, seed 1000+cfg)",
-        "config": {"workload": c["name"], "n_voxels": nv_total, "n_sites": ns,
-                   "parallelism": f"z-slab x{world}" + (f" + {args.dist_backend.upper()} histogram all-reduce"
-                                                          if world > 1 else ""),
-                   "l2": "flushed between steps (256 MB write); labels 4 B/voxel > L2",
-                   "labels": "int32 in HBM", "histogram": "uint64 grain volumes",
-                   "launch": "per-step C-ABI call" if args.no_graph else
-                             "CUDA-graph replay of the captured per-step pipeline"},
+        "config": config_dict(c, world),
+        "launch": ("per-step C-ABI call" if args.no_graph else
+                   "CUDA-graph replay of the captured per-step pipeline") +
+                  (f" + {args.dist_backend.upper()} histogram all-reduce" if world > 1 else ""),
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": launches,
@@ -390,10 +506,6 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="per-step C-ABI calls instead of CUDA-graph replays")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-planes", type=int, default=320)  # ~10 s of reference CPU work at cfg5
-    # 320 planes: the sampled rate matches a full reference run on the box (fixed per-call costs amortised)
-    ap.add_argument("--ref-planes", type=int, default=320)
-    ap.add_argument("--ref-budget-s", type=float, default=200.0)
     # functional dry run of the N > 1 path on a one-GPU box (not a measurement):
     # gloo collectives, every rank on cuda:0
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"], help=argparse.SUPPRESS)

@@ -94,8 +94,8 @@ def ref():
         L.vxref_search_optimal_t0.restype = _D
         L.vxref_validate_partition.argtypes = [C.c_int, C.c_int, C.c_int, _P, _P, _I64, _P, _P, _D,
                                                _P, _P, _I64, C.c_uint64, _P]
-        L.vxref_slab_sample.argtypes = [C.c_int, C.c_int, C.c_int, _P, _P, _I64, _P, _P, _D,
-                                        _I64, _I64, C.c_int, _P, _P]
+        L.vxref_tessellate_timed.argtypes = [C.c_int, C.c_int, C.c_int, _P, _P, _I64, _P, _P, _D,
+                                             C.c_int, _P, _P, _P, _P]
         L.vxref_max_threads.restype = C.c_int
         L.vxref_have_image_io.restype = C.c_int
         if L.vxref_have_image_io():
@@ -232,16 +232,31 @@ def ref_search_optimal_t0(p: Problem):
                                          _ptr(p.times), p.growth)
 
 
-def ref_slab_sample(p: Problem, z0, z1, threads=0):
-    plane = p.n_voxels // int(p.counts[-1])
-    lab = np.empty((z1 - z0) * plane, dtype=np.uint32)
+def ref_tessellate_timed(p: Problem, threads=0, labels=False):
+    """One stock tessellate_fast(sites, grid, FastOptions{}) call of the
+    reference library, timed around the call alone.  Returns (seconds,
+    fingerprint hex, param, labels or None)."""
+    lab = np.empty(p.n_voxels, dtype=np.uint32) if labels else None
+    sec = np.zeros(1)
+    fp = np.zeros(1, dtype=np.uint64)
     param = np.zeros(1)
-    rc = ref().vxref_slab_sample(p.kind, p.dim, int(p.periodic), _ptr(p.counts), _ptr(p.lengths),
-                                 p.n_sites, _ptr(p.positions), _ptr(p.times), p.growth, z0, z1,
-                                 threads, _ptr(lab), _ptr(param))
+    rc = ref().vxref_tessellate_timed(p.kind, p.dim, int(p.periodic), _ptr(p.counts), _ptr(p.lengths),
+                                      p.n_sites, _ptr(p.positions), _ptr(p.times), p.growth, threads,
+                                      _ptr(lab), _ptr(sec), _ptr(fp), _ptr(param))
     if rc:
-        raise RuntimeError(ref().vxref_last_error().decode())
-    return lab, float(param[0])
+        raise (ValueError if rc == 1 else RuntimeError)(ref().vxref_last_error().decode())
+    return float(sec[0]), "%016x" % int(fp[0]), float(param[0]), lab
+
+
+def ref_spheres_to_timed(positions, radii, growth, dim=3):
+    """The reference's spheres_to_timed_sites (sites.cpp:87-104): birth times."""
+    radii = np.ascontiguousarray(radii, dtype=np.float64)
+    positions = np.ascontiguousarray(positions, dtype=np.float64)
+    t = np.empty_like(radii)
+    rc = ref().vxref_spheres_to_timed(dim, radii.size, _ptr(positions), _ptr(radii), float(growth), _ptr(t))
+    if rc:
+        raise ValueError(ref().vxref_last_error().decode())
+    return t
 
 
 def ref_have_image_io() -> bool:

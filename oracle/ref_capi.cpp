@@ -14,11 +14,11 @@
 //   write/read_label_image, write/read_distance_image
 //                                        include/voxellate/image_io.hpp:24-29
 //                                        (only when built with VXREF_IMAGE_IO)
-// vxref_slab_sample() re-drives the reference's own step-1 window scan
-// (detail::for_each_window_voxel, ball_scan.hpp:55-124) and step-2 full scan
-// for one z-slab, with the reference's param choice, so that bench.py can
-// time a bounded sample of a 10^9-voxel run.
+// vxref_tessellate_timed() is the stock tessellate_fast with default options,
+// timed around the call alone: bench.py's reference arm and cpu_baseline.
 #include <omp.h>
+
+#include <chrono>
 
 #include <cstdint>
 #include <cstring>
@@ -28,7 +28,6 @@
 #include <vector>
 
 #include "voxellate/cost.hpp"
-#include "voxellate/detail/ball_scan.hpp"
 #include "voxellate/geometry.hpp"
 #include "voxellate/sites.hpp"
 #include "voxellate/tessellate.hpp"
@@ -117,6 +116,38 @@ int vxref_tessellate(int engine, int kind, int dim, int periodic, const int64_t*
   });
 }
 
+// bench.py --impl reference / cpu_baseline: one stock tessellate_fast call
+// (default FastOptions: prune on, model-optimal r0 / t0) timed around the call
+// alone (steady_clock), so neither the input copies into the reference's
+// SiteSet nor the output copies below are charged to it.  labels_out may be
+// NULL; fingerprint_out (may be NULL) receives the SURVEY.md App. B label
+// fingerprint of the result.
+int vxref_tessellate_timed(int kind, int dim, int periodic, const int64_t* counts,
+                           const double* lengths, int64_t n_sites, const double* positions,
+                           const double* times, double growth, int threads, uint32_t* labels_out,
+                           double* seconds_out, uint64_t* fingerprint_out, double* param_out) {
+  return guarded([&] {
+    if (threads > 0) omp_set_num_threads(threads);
+    const VoxelGrid grid = make_grid(dim, periodic, counts, lengths);
+    const SiteSet sites = make_sites(kind, dim, n_sites, positions, times, growth);
+    const auto t0 = std::chrono::steady_clock::now();
+    TessResult r = tessellate_fast(sites, grid, FastOptions{});
+    const auto t1 = std::chrono::steady_clock::now();
+    if (seconds_out) *seconds_out = std::chrono::duration<double>(t1 - t0).count();
+    if (param_out) *param_out = r.param;
+    const std::vector<uint32_t>& lab = r.labels.labels;
+    if (labels_out) std::memcpy(labels_out, lab.data(), lab.size() * sizeof(uint32_t));
+    if (fingerprint_out) {
+      uint64_t h = 1469598103934665603ull;
+      for (uint32_t l : lab) {
+        h ^= l;
+        h *= 1099511628211ull;
+      }
+      *fingerprint_out = h;
+    }
+  });
+}
+
 // Returns the number of removed sites (>= 0) or -1 on error; dropped_out[s]=1
 // for removed sites.
 int64_t vxref_prune(int kind, int dim, int periodic, const double* lengths, int64_t n_sites,
@@ -200,122 +231,6 @@ int vxref_validate_partition(int kind, int dim, int periodic, const int64_t* cou
     report_out[2] = rep.value_mismatches;
     report_out[3] = static_cast<int64_t>(rep.examples.size());
     for (size_t i = 0; i < rep.examples.size() && i < 16; ++i) report_out[4 + i] = rep.examples[i];
-  });
-}
-
-// Bounded CPU sample for bench.py: the reference's tessellate_fast work for
-// the voxels of last-axis slab [z0, z1) only.  Same parameter choice
-// (tessellate.cpp:217-260, incl. prune for timed kinds), same step-1 window
-// scan with slab bounds (tessellate.cpp:103-144 / ball_scan.hpp), same
-// unassigned-voxel full scan (tessellate.cpp:36-75) and Voronoi sqrt pass.
-// labels_out holds nx*ny*(z1-z0) entries; labels are original site indices.
-int vxref_slab_sample(int kind, int dim, int periodic, const int64_t* counts,
-                      const double* lengths, int64_t n_sites, const double* positions,
-                      const double* times, double growth, int64_t z0, int64_t z1, int threads,
-                      uint32_t* labels_out, double* param_out) {
-  return guarded([&] {
-    if (threads > 0) omp_set_num_threads(threads);
-    const VoxelGrid grid = make_grid(dim, periodic, counts, lengths);
-    const SiteSet all = make_sites(kind, dim, n_sites, positions, times, growth);
-    all.validate(grid.domain);
-    const SiteSet* work = &all;
-    SiteSet pruned;
-    std::vector<int64_t> kept;
-    if (all.timed()) {
-      PruneResult pr = prune_ineffective_sites(all, grid.domain);
-      if (!pr.removed.empty()) {
-        pruned = std::move(pr.sites);
-        kept = std::move(pr.kept);
-        work = &pruned;
-      }
-    }
-    const int64_t ns = work->count();
-    double param, cutoff;
-    std::vector<double> radii(static_cast<size_t>(ns));
-    if (all.kind == Kind::Voronoi) {
-      if (ns == 1) {  // cover_radius, tessellate.cpp:25-30
-        double s = 0.0;
-        for (double L : grid.domain.lengths) s += L * L;
-        param = grid.domain.periodic() ? 0.5 * std::sqrt(s) : std::sqrt(s);
-      } else {
-        param = radius_from_volume(optimal_v0(ns, grid.domain.volume()), grid.dim());
-      }
-      cutoff = param * param;
-      std::fill(radii.begin(), radii.end(), param);
-    } else {
-      param = ns == 1 ? t0_bracket(*work, grid.domain).hi : search_optimal_t0(*work, grid);
-      cutoff = param;
-      for (int64_t s = 0; s < ns; ++s) {
-        const double dt = param - work->times[s];
-        radii[s] = dt < 0.0 ? -1.0
-                            : (all.kind == Kind::JohnsonMehl ? work->growth * dt
-                                                             : std::sqrt(work->growth * dt));
-      }
-    }
-    if (param_out) *param_out = param;
-
-    const int d = grid.dim();
-    const int64_t plane = grid.voxel_count() / grid.counts[d - 1];
-    const int64_t base = z0 * plane;
-    const int64_t nvs = (z1 - z0) * plane;
-    std::vector<uint32_t> lab(static_cast<size_t>(nvs), kUnassignedLabel);
-    std::vector<double> val(static_cast<size_t>(nvs), std::numeric_limits<double>::infinity());
-    const double G = work->growth;
-    const Kind K = all.kind;
-
-#pragma omp parallel
-    {
-      const int tid = omp_get_thread_num();
-      const int nth = omp_get_num_threads();
-      const int64_t lo = z0 + (z1 - z0) * tid / nth;
-      const int64_t hi = z0 + (z1 - z0) * (tid + 1) / nth;
-      if (lo < hi) {
-        detail::ScanScratch scratch;
-        for (int64_t s = 0; s < ns; ++s) {
-          if (radii[s] < 0.0) continue;
-          const double ts = K == Kind::Voronoi ? 0.0 : work->times[s];
-          const uint32_t l = static_cast<uint32_t>(s);
-          detail::for_each_window_voxel(work->pos(s), radii[s], grid, lo, hi, scratch,
-                                        [&](int64_t lin, double dsq) {
-                                          const double prox = proximity_from_dsq(K, dsq, G, ts);
-                                          if (prox <= cutoff && prox < val[lin - base]) {
-                                            val[lin - base] = prox;
-                                            lab[lin - base] = l;
-                                          }
-                                        });
-        }
-      }
-    }
-    const double* L = grid.domain.lengths.data();
-    const double* iL = grid.domain.inv_lengths.data();
-#pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < nvs; ++i) {
-      if (lab[i] != kUnassignedLabel) continue;
-      int64_t idx[kMaxDim];
-      double x[kMaxDim];
-      grid.decompose(base + i, idx);
-      grid.center(idx, x);
-      double best = std::numeric_limits<double>::infinity();
-      uint32_t bl = kUnassignedLabel;
-      for (int64_t s = 0; s < ns; ++s) {
-        const double dsq = grid.domain.periodic() ? l_periodic_distance_sq(x, work->pos(s), d, L, iL)
-                                                  : euclidean_distance_sq(x, work->pos(s), d);
-        const double prox = proximity_from_dsq(K, dsq, G, K == Kind::Voronoi ? 0.0 : work->times[s]);
-        if (prox < best) {
-          best = prox;
-          bl = static_cast<uint32_t>(s);
-        }
-      }
-      lab[i] = bl;
-      val[i] = best;
-    }
-    if (K == Kind::Voronoi) {
-#pragma omp parallel for schedule(static)
-      for (int64_t i = 0; i < nvs; ++i) val[i] = std::sqrt(val[i]);
-    }
-#pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < nvs; ++i)
-      labels_out[i] = kept.empty() ? lab[i] : static_cast<uint32_t>(kept[lab[i]]);
   });
 }
 

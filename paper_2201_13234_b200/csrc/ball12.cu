@@ -213,14 +213,14 @@ __device__ __forceinline__ long long wrapi2(long long c, long long m) {
 template <int KIND, bool PER, bool DENSE>
 __global__ void __launch_bounds__(kB2Threads, 4)
     cull12_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, int2* __restrict__ info,
-                  int* __restrict__ slots16, int* __restrict__ list, long long list_cap, int* __restrict__ list_count,
-                  int* __restrict__ ovf,
-                  DevCounters* ctr, unsigned long long* __restrict__ eval_slots, int nbb) {
+                  int* __restrict__ slots16, int* __restrict__ list, long long list_cap,
+                  unsigned long long* __restrict__ list_count, int* __restrict__ ovf,
+                  DevCounters* ctr, unsigned long long* __restrict__ eval_slots, int nbb, unsigned by0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem2& S = *reinterpret_cast<Smem2*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
-  const long long K0[3] = {(long long)blockIdx.x * kSB, (long long)blockIdx.y * kSB,
+  const long long K0[3] = {(long long)blockIdx.x * kSB, (long long)(by0 + blockIdx.y) * kSB,
                            g.z_begin + (long long)blockIdx.z * (16 * nbb)};
   int ext[3];
   ext[0] = (int)min((long long)kSB, g.n[0] - K0[0]);
@@ -635,10 +635,12 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       }
       __syncwarp();
       const long long sbi = sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz);
-      int base = 0;
-      if (lane == 0 && n2 > kSlot && n2 <= kLcapD) base = atomicAdd(list_count, n2);
+      // 64-bit list offsets: the counter keeps growing past list_cap, and
+      // only offsets with base + n2 <= list_cap (< 2^31) are ever written
+      long long base = 0;
+      if (lane == 0 && n2 > kSlot && n2 <= kLcapD) base = (long long)atomicAdd(list_count, (unsigned long long)n2);
       base = __shfl_sync(0xffffffffu, base, 0);
-      const bool ok = n2 <= kLcapD && (n2 <= kSlot || (long long)base + n2 <= list_cap);
+      const bool ok = n2 <= kLcapD && (n2 <= kSlot || base + n2 <= list_cap);
       if (ok) {
         int* dst = n2 <= kSlot ? slots16 + sbi * kSlot : list + base;
         for (int i = lane; i < n2; i += 32) dst[i] = ws.L[i];
@@ -650,7 +652,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
         atomicMax(&eval_slots[73], (unsigned long long)n2);
       }
       if (lane == 0) {
-        info[sbi] = ok ? make_int2(base, n2) : make_int2(0, -1);
+        info[sbi] = ok ? make_int2((int)base, n2) : make_int2(0, -1);
         if (!ok) ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sbi;
         if (ok) ws.evals += (unsigned)(n2 * sext[0] * sext[1] * sext[2]);
       }
@@ -697,10 +699,10 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       const long long sbi = sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz);
       const unsigned ma = __ballot_sync(0xffffffffu, ka), mb = __ballot_sync(0xffffffffu, kb);
       n2 = __popc(ma) + __popc(mb);
-      int base = 0;
-      if (lane == 0 && n2 > kSlot && n2 <= kLcap) base = atomicAdd(list_count, n2);
+      long long base = 0;
+      if (lane == 0 && n2 > kSlot && n2 <= kLcap) base = (long long)atomicAdd(list_count, (unsigned long long)n2);
       base = __shfl_sync(0xffffffffu, base, 0);
-      const bool ok = n2 <= kLcap && (n2 <= kSlot || (long long)base + n2 <= list_cap);
+      const bool ok = n2 <= kLcap && (n2 <= kSlot || base + n2 <= list_cap);
       if (ok) {
         const unsigned lt = (1u << lane) - 1u;
         int* dst = n2 <= kSlot ? slots16 + sbi * kSlot : list + base;
@@ -713,7 +715,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
         atomicMax(&eval_slots[73], (unsigned long long)n2);
       }
       if (lane == 0) {
-        info[sbi] = ok ? make_int2(base, n2) : make_int2(0, -1);
+        info[sbi] = ok ? make_int2((int)base, n2) : make_int2(0, -1);
         if (!ok) ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sbi;
         if (ok && n2 <= kFcap) ws.evals += (unsigned)(n2 * sext[0] * sext[1] * sext[2]);
       }
@@ -1044,7 +1046,7 @@ template <int KIND, bool PER, bool DENSE>
 static int launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* labels, double* dist,
                      unsigned long long* hist, long long* unres, long long cap, DevCounters* ctr,
                      unsigned long long* slots, int2* info, int* slots16, int* list, long long list_cap,
-                     int* list_count, int* ovf, int nbb, cudaStream_t st) {
+                     unsigned long long* list_count, int* ovf, int nbb, cudaStream_t st) {
   // the dynamic-smem opt-in is per device: remember it per device ordinal
   static std::atomic<unsigned long long> attr_done{0};
   int dev = 0;
@@ -1061,13 +1063,18 @@ static int launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* l
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_e);
     attr_done.fetch_or(bit);
   }
-  const dim3 grid((unsigned)((g.n[0] + v12::kSB - 1) / v12::kSB), (unsigned)((g.n[1] + v12::kSB - 1) / v12::kSB),
-                  (unsigned)((g.z_end - g.z_begin + 16 * nbb - 1) / (16 * nbb)));
-  v12::cull12_kernel<KIND, PER, DENSE><<<grid, v12::kB2Threads, sh_c, st>>>(g, bins, prm, info, slots16, list, list_cap,
-                                                                     list_count, ovf, ctr, slots, nbb);
+  int launches = 0;
+  // super-brick rows along y in chunks of gridDim.y <= 65535
+  const long long sbrows = (g.n[1] + v12::kSB - 1) / v12::kSB;
+  for (long long y0 = 0; y0 < sbrows; y0 += v12::kMaxGridY, ++launches) {
+    const dim3 grid((unsigned)((g.n[0] + v12::kSB - 1) / v12::kSB),
+                    (unsigned)std::min<long long>(v12::kMaxGridY, sbrows - y0),
+                    (unsigned)((g.z_end - g.z_begin + 16 * nbb - 1) / (16 * nbb)));
+    v12::cull12_kernel<KIND, PER, DENSE><<<grid, v12::kB2Threads, sh_c, st>>>(
+        g, bins, prm, info, slots16, list, list_cap, list_count, ovf, ctr, slots, nbb, (unsigned)y0);
+  }
   const long long nsb = ball12_subbricks(g);
   const long long rows = ((g.n[1] + 7) / 8 + v12::kEvalWarps - 1) / v12::kEvalWarps;  // CTA rows along y
-  int launches = 0;
   for (long long r0 = 0; r0 < rows; r0 += v12::kMaxGridY, ++launches) {
     const dim3 eg((unsigned)((g.n[0] + 7) / 8), (unsigned)std::min<long long>(v12::kMaxGridY, rows - r0),
                   (unsigned)((g.z_end - g.z_begin + 3) / 4));
@@ -1080,17 +1087,17 @@ static int launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* l
           g, bins, prm, info, slots16, list, labels, dist, hist, unres, cap, ctr, slots, nsb, sby0);
   }
   launch_subshell(g, bins, prm, ovf, &ctr->n_ovf_sb, labels, dist, hist, ctr, st);
-  return launches - 1;  // eval launches beyond the first
+  return launches - 2;  // cull / eval launches beyond the first of each
 }
 
 int launch_ball12(const Geo& g, const Bins& bins, const DevParams* prm, int* labels, double* dist,
                   unsigned long long* hist, long long* unres, long long unres_cap, DevCounters* ctr,
                   unsigned long long* slots, int2* info, int* slots16, int* list, long long list_cap,
-                  int* list_count, int* ovf, cudaStream_t st) {
+                  unsigned long long* list_count, int* ovf, cudaStream_t st) {
   if (g.z_end <= g.z_begin) return 0;
   cudaMemsetAsync(&ctr->n_ovf_sb, 0, sizeof(unsigned long long), st);
   cudaMemsetAsync(slots, 0, 128 * sizeof(unsigned long long), st);
-  cudaMemsetAsync(list_count, 0, sizeof(int), st);
+  cudaMemsetAsync(list_count, 0, sizeof(unsigned long long), st);
   static const int nbb_env = std::getenv("VX_NBB") ? std::atoi(std::getenv("VX_NBB")) : 0;
   const int nbb = nbb_env == 1 || nbb_env == 2 || nbb_env == 4 ? nbb_env : choose_nbb12(g);
   const bool dense = ball12_dense(g);

@@ -141,11 +141,12 @@ int launch_brute(int kind, int periodic, int dim, const long long* counts, const
 
 int launch_validate(int kind, int periodic, int dim, const long long* counts,
                     const double* lengths, double growth, const double* pos, const double* t,
-                    long long n_sites, const long long* sample, long long n_sample,
+                    long long n_sites, const long long* sample, long long lin_begin, long long n_sample,
                     const int* labels_at, const double* dist_at, int* bad_label, int* bad_value,
                     cudaStream_t st) {
   const BruteGeo g = make_bgeo(kind, periodic, dim, counts, lengths, growth);
-  dispatch(g, pos, t, n_sites, 0, n_sample, sample, nullptr, nullptr, nullptr, labels_at, dist_at,
+  // sample == nullptr: the contiguous voxel range [lin_begin, lin_begin + n_sample)
+  dispatch(g, pos, t, n_sites, lin_begin, n_sample, sample, nullptr, nullptr, nullptr, labels_at, dist_at,
            bad_label, bad_value, st);
   return 1;
 }

@@ -14,6 +14,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -43,6 +44,22 @@ int fail(int code, const std::string& msg) {
 }  // namespace
 
 void vxb::set_last_error(const std::string& msg) { g_err = msg; }
+
+int vxb::sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& c = cache[dev & 63];
+  int n = c.load();
+  if (n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148;
+    }
+    c.store(n);
+  }
+  return n;
+}
 
 namespace {
 
@@ -74,6 +91,13 @@ struct vx_context {
   void* pin[2] = {};                   // pinned double buffer of the file writer
   size_t pin_bytes = 0;
 
+  vx_context() = default;
+  vx_context(const vx_context&) = delete;
+  vx_context& operator=(const vx_context&) = delete;
+  // Frees every device / pinned resource: vx_context_destroy, the per-thread
+  // default contexts when their thread exits, and a failed create_context.
+  ~vx_context();
+
   Buf* all[35] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
                   &vals_a,  &vals_b,  &bx,    &by,    &bz,     &bt,      &bidx,     &cell_start,
                   &cub,     &labels,  &dist,  &hist,  &unres,  &params,  &counters, &scratch,
@@ -95,6 +119,43 @@ struct DeviceGuard {
     if (prev >= 0 && cur != prev) cudaSetDevice(prev);
   }
 };
+
+}  // namespace
+
+vx_context::~vx_context() {
+  // at process exit the CUDA runtime may already be unloading: then there is
+  // nothing left to free
+  int cur = -1;
+  if (cudaGetDevice(&cur) == cudaErrorCudartUnloading) return;
+  cudaGetLastError();
+  DeviceGuard guard(device);
+  if (stream) cudaStreamSynchronize(stream);
+  for (Buf* b : all)
+    if (b->p) {
+      cudaFree(b->p);
+      b->p = nullptr;
+      b->n = 0;
+    }
+  if (h_prm) cudaFreeHost(h_prm);
+  if (h_ctr) cudaFreeHost(h_ctr);
+  if (stream) cudaStreamDestroy(stream);
+  if (copy_stream) {
+    cudaStreamSynchronize(copy_stream);
+    cudaStreamDestroy(copy_stream);
+  }
+  for (auto e : chunk_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto e : sink_ev) cudaEventDestroy(e);
+  for (auto e : done_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto b : pin)
+    if (b) cudaFreeHost(b);
+  for (auto e : ev)
+    if (e) cudaEventDestroy(e);
+  cudaGetLastError();
+}
+
+namespace {
 
 struct CudaFail {
   int code;
@@ -742,25 +803,18 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       trace.rec(5, st);
       dbg(st, "params");
       tm.mark(3);
-      static const int ball_ver = std::getenv("VX_BALL") ? std::atoi(std::getenv("VX_BALL")) : 12;
       auto ball_and_shell = [&](const Geo& gg, int32_t* lb, double* ds) {
         unsigned long long* slots = ensure<unsigned long long>(ctx->slots, 128);
-        if (ball_ver == 12) {
-          const long long nsb = ball12_subbricks(gg);
-          int2* info = ensure<int2>(ctx->sb_info, (size_t)nsb);
-          int* slots16 = ensure<int>(ctx->sb_slots, (size_t)nsb * 16);
-          const long long lcap =  // lists > 16 only (dense mode: most of them)
-              std::min<long long>(nsb * (ball12_dense(gg) ? 48 : 4) + (1 << 20), (1ll << 31) - 1);
-          int* list = ensure<int>(ctx->sb_list, (size_t)lcap);
-          int* lcount = ensure<int>(ctx->sb_count, 1);
-          int* ovf = ensure<int>(ctx->sb_ovf, (size_t)nsb);
-          launches += launch_ball12(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, info, slots16, list, lcap,
-                                    lcount, ovf, st);
-        } else if (ball_ver == 11) {
-          launches += launch_ball11(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, st);
-        } else {
-          launches += launch_ball(gg, bins, prm, lb, ds, hist, unres, cap, ctr, st);
-        }
+        const long long nsb = ball12_subbricks(gg);
+        int2* info = ensure<int2>(ctx->sb_info, (size_t)nsb);
+        int* slots16 = ensure<int>(ctx->sb_slots, (size_t)nsb * 16);
+        const long long lcap =  // lists > 16 only (dense mode: most of them)
+            std::min<long long>(nsb * (ball12_dense(gg) ? 48 : 4) + (1 << 20), (1ll << 31) - 1);
+        int* list = ensure<int>(ctx->sb_list, (size_t)lcap);
+        unsigned long long* lcount = ensure<unsigned long long>(ctx->sb_count, 1);
+        int* ovf = ensure<int>(ctx->sb_ovf, (size_t)nsb);
+        launches += launch_ball12(gg, bins, prm, lb, ds, hist, unres, cap, ctr, slots, info, slots16, list, lcap,
+                                  lcount, ovf, st);
         dbg(st, "ball");
         tm.mark(4);
         launches += launch_shell(gg, bins, prm, lb, ds, hist, unres, cap, ctr, st);
@@ -966,6 +1020,7 @@ int run_multi(const vx_problem* P, const vx_options& O, int32_t* labels_out, vx_
       vx_options o = O;
       o.n_gpus = 1;
       o.device = dev;
+      o.stream = nullptr;  // a caller's stream belongs to one device: each rank uses its context's
       o.slab_begin = a;
       o.slab_end = b;
       o.distances_out = O.distances_out ? O.distances_out + (a - zb) * plane : nullptr;
@@ -987,8 +1042,12 @@ int run_multi(const vx_problem* P, const vx_options& O, int32_t* labels_out, vx_
       for (size_t i = 0; i < h.size(); ++i) O.histogram_out[i] += h[i];
   }
   if (stats) {
-    *stats = st[0];
-    for (int r = 1; r < G; ++r) {
+    // seed from the first rank that labelled a slab (ranks past the last
+    // plane get none and leave their stats zero)
+    int r0 = 0;
+    while (r0 < G - 1 && st[r0].n_voxels == 0) ++r0;
+    *stats = st[r0];
+    for (int r = r0 + 1; r < G; ++r) {
       stats->n_voxels += st[r].n_voxels;
       stats->n_unresolved += st[r].n_unresolved;
       stats->ball_evals += st[r].ball_evals;
@@ -1026,36 +1085,7 @@ int vx_context_create(int device, vx_context** out) {
   return create_context(device, out);
 }
 
-void vx_context_destroy(vx_context* ctx) {
-  if (!ctx) return;
-  {
-    DeviceGuard guard(ctx->device);
-    cudaStreamSynchronize(ctx->stream);
-    for (Buf* b : ctx->all)
-      if (b->p) {
-        cudaFree(b->p);
-        b->p = nullptr;
-        b->n = 0;
-      }
-    if (ctx->h_prm) cudaFreeHost(ctx->h_prm);
-    if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
-    cudaStreamDestroy(ctx->stream);
-    if (ctx->copy_stream) {
-      cudaStreamSynchronize(ctx->copy_stream);
-      cudaStreamDestroy(ctx->copy_stream);
-      for (auto e : ctx->chunk_ev)
-        if (e) cudaEventDestroy(e);
-    }
-    for (auto e : ctx->sink_ev) cudaEventDestroy(e);
-    for (auto e : ctx->done_ev)
-      if (e) cudaEventDestroy(e);
-    for (auto b : ctx->pin)
-      if (b) cudaFreeHost(b);
-    for (auto e : ctx->ev)
-      if (e) cudaEventDestroy(e);
-  }
-  delete ctx;
-}
+void vx_context_destroy(vx_context* ctx) { delete ctx; }
 
 int vx_context_stage_ms(vx_context* ctx, float* stage_ms) {
   if (!ctx || !stage_ms) return fail(VX_EINVAL, "context and stage_ms must not be NULL");
@@ -1186,29 +1216,23 @@ int vx_validate_partition(vx_context* ctx_in, const vx_problem* P, const int32_t
   const int d = P->dim;
   int64_t nv = 1;
   for (int i = 0; i < d; ++i) nv *= P->counts[i];
+  // tessellate.cpp:321-330: every voxel in order, or `sample` mt19937_64 draws
+  const bool all = sample <= 0 || sample >= nv;
   std::vector<long long> chosen;
-  if (sample <= 0 || sample >= nv) {  // tessellate.cpp:321-330
-    chosen.resize((size_t)nv);
-    for (int64_t i = 0; i < nv; ++i) chosen[i] = i;
-  } else {
+  if (!all) {
     std::mt19937_64 eng(seed);
     std::uniform_int_distribution<std::int64_t> pick(0, nv - 1);
     chosen.resize((size_t)sample);
     for (auto& c : chosen) c = pick(eng);
   }
-  const int64_t n = (int64_t)chosen.size();
-  std::vector<int> lab_at((size_t)n), bad_l((size_t)n, 0), bad_v((size_t)n, 0);
-  std::vector<double> dist_at(distances ? (size_t)n : 0);
-  for (int64_t i = 0; i < n; ++i) {
-    lab_at[i] = labels[chosen[i]];
-    if (distances) dist_at[i] = distances[chosen[i]];
-  }
+  const int64_t n = all ? nv : (int64_t)chosen.size();
   vx_context* ctx = resolve_context(ctx_in, nullptr, &rc);
   if (!ctx) return rc;
   std::lock_guard<std::mutex> lock(ctx->mu);
   DeviceGuard guard(ctx->device);
   cudaStream_t st = ctx->stream;
   const int64_t ns = P->n_sites;
+  std::memset(report, 0, sizeof(*report));
   try {
     double* pos = ensure<double>(ctx->pos_raw, (size_t)ns * d);
     ck(cudaMemcpyAsync(pos, P->positions, sizeof(double) * ns * d, cudaMemcpyHostToDevice, st), "H2D");
@@ -1226,30 +1250,47 @@ int vx_validate_partition(vx_context* ctx_in, const vx_problem* P, const int32_t
       launch_ingest(g, len, d, pos, P->times ? src : nullptr, P->times ? nullptr : src, nullptr, tdev,
                     ctr, st);
     }
-    long long* ds = ensure<long long>(ctx->vsample, (size_t)n);
-    int* dl = ensure<int>(ctx->vlab, (size_t)n);
-    double* dd = distances ? ensure<double>(ctx->vdist, (size_t)n) : nullptr;
-    int* bad = ensure<int>(ctx->vbad, (size_t)(2 * n));
-    ck(cudaMemcpyAsync(ds, chosen.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st), "H2D");
-    ck(cudaMemcpyAsync(dl, lab_at.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st), "H2D");
-    if (dd) ck(cudaMemcpyAsync(dd, dist_at.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st), "H2D");
-    ck(cudaMemsetAsync(bad, 0, sizeof(int) * 2 * n, st), "memset");
-    launch_validate(P->kind, P->periodic, d, reinterpret_cast<const long long*>(P->counts), P->lengths, timed(P) ? P->growth : 0.0, pos,
-                    tdev, ns, ds, n, dl, dd, bad, bad + n, st);
-    ck(cudaGetLastError(), "kernel launch");
-    ck(cudaMemcpyAsync(bad_l.data(), bad, sizeof(int) * n, cudaMemcpyDeviceToHost, st), "D2H");
-    ck(cudaMemcpyAsync(bad_v.data(), bad + n, sizeof(int) * n, cudaMemcpyDeviceToHost, st), "D2H");
-    ck(cudaStreamSynchronize(st), "validate");
+    // pieces of <= 2^24 voxels: device and host memory stay bounded whatever
+    // the image size (a full audit of a 10^9-voxel image never materialises
+    // grid-sized index arrays)
+    const int64_t piece = std::min<int64_t>(n, 1 << 24);
+    long long* ds = all ? nullptr : ensure<long long>(ctx->vsample, (size_t)piece);
+    int* dl = ensure<int>(ctx->vlab, (size_t)piece);
+    double* dd = distances ? ensure<double>(ctx->vdist, (size_t)piece) : nullptr;
+    int* bad = ensure<int>(ctx->vbad, (size_t)(2 * piece));
+    std::vector<int> lab_at(all ? 0 : (size_t)piece), bad_h((size_t)(2 * piece));
+    std::vector<double> dist_at(all || !distances ? 0 : (size_t)piece);
+    for (int64_t c0 = 0; c0 < n; c0 += piece) {
+      const int64_t m = std::min(piece, n - c0);
+      if (all) {  // the caller's contiguous range goes straight to the device
+        ck(cudaMemcpyAsync(dl, labels + c0, sizeof(int) * m, cudaMemcpyHostToDevice, st), "H2D");
+        if (dd) ck(cudaMemcpyAsync(dd, distances + c0, sizeof(double) * m, cudaMemcpyHostToDevice, st), "H2D");
+      } else {
+        for (int64_t i = 0; i < m; ++i) {
+          lab_at[i] = labels[chosen[c0 + i]];
+          if (distances) dist_at[i] = distances[chosen[c0 + i]];
+        }
+        ck(cudaMemcpyAsync(ds, chosen.data() + c0, sizeof(long long) * m, cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(dl, lab_at.data(), sizeof(int) * m, cudaMemcpyHostToDevice, st), "H2D");
+        if (dd) ck(cudaMemcpyAsync(dd, dist_at.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st), "H2D");
+      }
+      ck(cudaMemsetAsync(bad, 0, sizeof(int) * 2 * m, st), "memset");
+      launch_validate(P->kind, P->periodic, d, reinterpret_cast<const long long*>(P->counts), P->lengths,
+                      timed(P) ? P->growth : 0.0, pos, tdev, ns, ds, all ? c0 : 0, m, dl, dd, bad, bad + m, st);
+      ck(cudaGetLastError(), "kernel launch");
+      ck(cudaMemcpyAsync(bad_h.data(), bad, sizeof(int) * 2 * m, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "validate");
+      for (int64_t i = 0; i < m; ++i) {
+        ++report->voxels_checked;
+        const bool bl = bad_h[i] != 0, bv = distances && bad_h[m + i] != 0;
+        report->label_mismatches += bl;
+        report->value_mismatches += bv;
+        if ((bl || bv) && report->n_examples < 16)
+          report->examples[report->n_examples++] = all ? c0 + i : chosen[c0 + i];
+      }
+    }
   } catch (const CudaFail& f) {
     return fail(f.code, f.msg);
-  }
-  std::memset(report, 0, sizeof(*report));
-  for (int64_t i = 0; i < n; ++i) {
-    ++report->voxels_checked;
-    const bool bl = bad_l[i] != 0, bv = distances && bad_v[i] != 0;
-    report->label_mismatches += bl;
-    report->value_mismatches += bv;
-    if ((bl || bv) && report->n_examples < 16) report->examples[report->n_examples++] = chosen[i];
   }
   return VX_OK;
 }

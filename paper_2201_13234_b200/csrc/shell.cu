@@ -246,7 +246,7 @@ template <int KIND>
 static void launch_k(const Geo& g, const Bins& bins, const DevParams* prm, int* labels,
                      double* dist, unsigned long long* hist, const long long* unres,
                      long long cap, DevCounters* ctr, cudaStream_t st) {
-  const int blocks = 148 * 4;
+  const int blocks = sm_count() * 4;
   if (g.periodic)
     shell_kernel<KIND, true><<<blocks, kShellThreads, 0, st>>>(g, bins, prm, labels, dist, hist,
                                                                unres, cap, ctr);

@@ -217,7 +217,7 @@ int launch_subshell(const Geo& g, const Bins& bins, const DevParams* prm, const 
                     const unsigned long long* n_ovf, int* labels, double* dist, unsigned long long* hist,
                     DevCounters* ctr, cudaStream_t st) {
   if (g.z_end <= g.z_begin) return 0;
-  const unsigned blocks = 148 * 8;  // persistent warps walk the overflow list
+  const unsigned blocks = (unsigned)sm_count() * 8;  // persistent warps walk the overflow list
 #define VX_SS(K, P) \
   ssh::subshell_kernel<K, P><<<blocks, ssh::kThreads, 0, st>>>(g, bins, prm, ovf, n_ovf, labels, dist, hist, ctr)
   switch (g.kind * 2 + (g.periodic ? 1 : 0)) {

@@ -55,13 +55,20 @@ def tessellate_slabs(sites, grid, options=None, *, group=None, gather: bool = Fa
     n_last = grid.counts[-1]
     z0, z1 = slab_bounds(n_last, rank, world)
     lab = labeller or (lambda s, g, o, sl: gpu_labeller(s, g, o, sl, device))
-    labels, hist = lab(sites, grid, options, (z0, z1))
+    if z1 > z0:
+        labels, hist = lab(sites, grid, options, (z0, z1))
+    else:  # more ranks than planes: nothing to label, but join every collective
+        labels = np.empty(0, dtype=np.uint32)
+        hist = np.zeros(sites.count(), dtype=np.int64)
     hist = np.asarray(hist, dtype=np.int64)
+    # NCCL tensors live on this rank's GPU (the given device, else the current one)
+    cuda_dev = None
+    if world > 1 and dist.get_backend(group) == "nccl":
+        cuda_dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
     if world > 1:
-        use_cuda = dist.get_backend(group) == "nccl"
         t = torch.from_numpy(hist.copy())
-        if use_cuda:
-            t = t.cuda()
+        if cuda_dev is not None:
+            t = t.to(cuda_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
         hist = t.cpu().numpy()
     image = None
@@ -75,9 +82,8 @@ def tessellate_slabs(sites, grid, options=None, *, group=None, gather: bool = Fa
             mx = max(sizes)
             buf = torch.full((mx,), -1, dtype=torch.int32)
             buf[: labels.size] = torch.from_numpy(np.asarray(labels).view(np.int32))
-            use_cuda = dist.get_backend(group) == "nccl"
-            if use_cuda:
-                buf = buf.cuda()
+            if cuda_dev is not None:
+                buf = buf.to(cuda_dev)
             outs = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
             dist.gather(buf, outs, dst=0, group=group)
             if rank == 0:

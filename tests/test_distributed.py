@@ -25,12 +25,12 @@ def _free_port():
     return p
 
 
-def _problem():
+def _problem(nz=17):
     sys.path.insert(0, ROOT)
     import oracle
 
     pos, t = oracle.generate_uniform_sites(3, np.array([1.0, 0.8, 1.2]), 200, 1, 0.05, 77)
-    return oracle.Problem(1, [13, 11, 17], [1.0, 0.8, 1.2], True, pos, t, 1.3)
+    return oracle.Problem(1, [13, 11, nz], [1.0, 0.8, 1.2], True, pos, t, 1.3)
 
 
 def _oracle_labeller(p):
@@ -45,7 +45,7 @@ def _oracle_labeller(p):
     return lab
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, nz):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         sys.path.insert(0, ROOT)
@@ -55,7 +55,7 @@ def _worker(rank, world, port, q):
         from paper_2201_13234_b200.distributed import tessellate_slabs
 
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        p = _problem()
+        p = _problem(nz)
         sites, grid = to_vx(p)
         res = tessellate_slabs(sites, grid, gather=True, labeller=_oracle_labeller(p))
         q.put((rank, res.z0, res.z1, res.histogram, res.image))
@@ -64,12 +64,14 @@ def _worker(rank, world, port, q):
         q.put((rank, "error", repr(e), None, None))
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_slab_decomposition_gloo(world):
+@pytest.mark.parametrize("world,nz", [(2, 17), (3, 17), (3, 2)])
+def test_slab_decomposition_gloo(world, nz):
+    """nz = 2 < world = 3: the rank without planes joins every collective with
+    an empty slab and a zero histogram (no hang, same reduced result)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, nz)) for r in range(world)]
     for pr in procs:
         pr.start()
     got = [q.get(timeout=240) for _ in range(world)]
@@ -81,7 +83,7 @@ def test_slab_decomposition_gloo(world):
     sys.path.insert(0, ROOT)
     import oracle
 
-    p = _problem()
+    p = _problem(nz)
     full, _ = oracle.brute(p, distances=False)
     hist = np.bincount(full, minlength=p.n_sites)
     n = int(p.counts[-1])
