@@ -742,19 +742,16 @@ __device__ __forceinline__ void exact_tables(ES& ws, const Bins& bins, const Geo
     const int a = e >= 2 * m ? 2 : (e >= m ? 1 : 0);
     const int j = e - a * m;
     const int p = ws.P[c0 + j];
-    const double* sa = a == 0 ? bins.x : (a == 1 ? bins.y : bins.z);
-    const double sv = sa[p];
+    const double sv = bins.x[p + a * bins.stride];  // x, y, z arrays are contiguous
     const double* cr = &ws.C[a * 8];
     double u[8];
-    bool far = false;
     const double La = PER ? (a == 0 ? g.L[0] : (a == 1 ? g.L[1] : g.L[2])) : 0.0;
     const double lim = 0.49 * La;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      u[r] = __dsub_rn(sv, cr[r]);
-      if (PER) far |= !(fabs(u[r]) < lim);
-    }
-    if (PER && far) {  // rare: a site about half a period away
+    for (int r = 0; r < 8; ++r) u[r] = __dsub_rn(sv, cr[r]);
+    // u is monotone in the (increasing) centres: |u| peaks at an end (for z
+    // the 4th centre repeats as entries 4..7 when a sub-brick is short)
+    if (PER && (!(fabs(u[0]) < lim) || !(fabs(u[7]) < lim) || !(fabs(u[3]) < lim))) {  // rare: ~half a period away
       const double iLa = a == 0 ? g.invL[0] : (a == 1 ? g.invL[1] : g.invL[2]);
 #pragma unroll
       for (int r = 0; r < 8; ++r)
@@ -801,8 +798,9 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 32 / kEvalWarps)
   const int pl = inf.y > kSlot ? (lane < inf.y ? list[inf.x + lane] : 0) : ps;
   if (inf.y < 0) return;  // overflowed the ball phase's caps: the sub-brick shell labels it
   {
-    const long long x0 = (long long)sbx * 8, y0 = (long long)sby * 8, z0 = g.z_begin + (long long)sbz * 4;
-    const int sext[3] = {(int)min(8ll, g.n[0] - x0), (int)min(8ll, g.n[1] - y0), (int)min(4ll, g.z_end - z0)};
+    const int x0 = (int)sbx * 8, y0 = (int)sby * 8;
+    const long long z0 = g.z_begin + (long long)sbz * 4;
+    const int sext[3] = {min(8, (int)g.n[0] - x0), min(8, (int)g.n[1] - y0), (int)min(4ll, g.z_end - z0)};
     // lists longer than the tables (a few per image at the benchmark densities)
     // send their voxels to the per-voxel shell search
     const int n2 = inf.y <= (DENSE ? kLcapD : kFcap) ? inf.y : 0;
@@ -825,8 +823,10 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 32 / kEvalWarps)
     }
     if (lane < 24 && n2 > 0) {  // the sub-brick's voxel centres, once (geometry.hpp:58-60)
       const int a = lane >> 3;
-      const long long k0 = a == 0 ? x0 : (a == 1 ? y0 : z0);
-      ws.C[lane] = center(k0 + (lane & 7), a == 0 ? g.sp[0] : (a == 1 ? g.sp[1] : g.sp[2]));
+      // beyond the grid the last centre repeats (never stored); z entries 4..7 repeat the 4th
+      const int k = min(lane & 7, (a == 0 ? sext[0] : (a == 1 ? sext[1] : sext[2])) - 1);
+      const long long k0 = a == 0 ? (long long)x0 : (a == 1 ? (long long)y0 : z0);
+      ws.C[lane] = center(k0 + k, a == 0 ? g.sp[0] : (a == 1 ? g.sp[1] : g.sp[2]));
     }
     __syncwarp();
     auto store_tail = [&](double (&best)[8], int (&bj)[8]) {
@@ -908,7 +908,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 32 / kEvalWarps)
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         best[k] = __longlong_as_double(0x7ff0000000000000ll);
-        bj[k] = -1;
+        bj[k] = 0;  // any in-range slot: unresolved voxels never read it
       }
       const bool g1 = g.g_is_one;
       // candidates in passes of kFcap tables; the running minimum carries
@@ -950,7 +950,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 32 / kEvalWarps)
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       best[k] = __longlong_as_double(0x7ff0000000000000ll);
-      bj[k] = -1;
+      bj[k] = 0;  // any in-range slot: unresolved voxels never read it
     }
     const bool g1 = g.g_is_one;
     for (int j = 0; j < n2; ++j) {

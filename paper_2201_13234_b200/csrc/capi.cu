@@ -79,7 +79,7 @@ struct vx_context {
   std::mutex mu;
   Buf pos_raw, t_raw, w_raw, p3, t, dropped, keys_a, keys_b, vals_a, vals_b, bx, by, bz, bt, bidx,
       cell_start, cub, labels, dist, hist, unres, params, counters, scratch, vsample, vlab, vdist,
-      vbad, slots, f4, sb_info, sb_list, sb_count, sb_slots, sb_ovf;
+      vbad, slots, f4, sb_info, sb_list, sb_count, sb_slots, sb_ovf, ctab;
   DevParams* h_prm = nullptr;
   DevCounters* h_ctr = nullptr;
   cudaEvent_t ev[8] = {};  // stage markers (options.profile_stages)
@@ -98,11 +98,11 @@ struct vx_context {
   // default contexts when their thread exits, and a failed create_context.
   ~vx_context();
 
-  Buf* all[35] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
+  Buf* all[36] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
                   &vals_a,  &vals_b,  &bx,    &by,    &bz,     &bt,      &bidx,     &cell_start,
                   &cub,     &labels,  &dist,  &hist,  &unres,  &params,  &counters, &scratch,
                   &vsample, &vlab,    &vdist, &vbad,  &slots,  &f4,      &sb_info,  &sb_list,
-                  &sb_count, &sb_slots, &sb_ovf};
+                  &sb_count, &sb_slots, &sb_ovf, &ctab};
 };
 
 namespace {
@@ -701,6 +701,17 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
     }
     Geo g;
     fill_geo(g, P, zb, ze, ns, xy2d);
+    if (!use_brute) {  // exact voxel centres per axis (<= 4 Mi entries; else computed inline)
+      const long long tot = g.n[0] + g.n[1] + g.n[2];
+      if (tot <= (4ll << 20)) {
+        g.ctab_off[0] = 0;
+        g.ctab_off[1] = g.n[0];
+        g.ctab_off[2] = g.n[0] + g.n[1];
+        double* ct = ensure<double>(ctx->ctab, (size_t)tot);
+        g.ctab = ct;
+        launches += launch_centres(g, ct, st);
+      }
+    }
     int32_t* lab = host_io ? ensure<int32_t>(ctx->labels, (size_t)nvs) : labels_out;
     double* dist = nullptr;
     // host-buffer call into pageable memory: stage through pinned buffers
@@ -761,9 +772,10 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       if (sink) sink_chunks.push_back({zb, ze, sink_event(ctx, 0, st)});
     } else {
       Bins bins;
-      double* bx = ensure<double>(ctx->bx, (size_t)ns);
-      double* by = ensure<double>(ctx->by, (size_t)ns);
-      double* bz = ensure<double>(ctx->bz, (size_t)ns);
+      // binned x, y, z in one allocation (the eval kernels index x + a * ns)
+      double* bx = ensure<double>(ctx->bx, (size_t)ns * 3);
+      double* by = bx + ns;
+      double* bz = bx + 2 * ns;
       double* bt = timed(P) ? ensure<double>(ctx->bt, (size_t)ns) : nullptr;
       int* bidx = ensure<int>(ctx->bidx, (size_t)ns);
       int* cs = ensure<int>(ctx->cell_start, (size_t)g.n_cells + 1);
@@ -780,6 +792,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       bins.x = bx;
       bins.y = by;
       bins.z = bz;
+      bins.stride = ns;
       bins.t = bt;
       bins.idx = bidx;
       bins.cell_start = cs;
@@ -1174,9 +1187,9 @@ int vx_prune(vx_context* ctx_in, const vx_problem* P, uint8_t* dropped_out, int6
     launch_ingest(g, len, d, pos, P->times ? src : nullptr, P->times ? nullptr : src, p3, tdev, ctr, st);
     if (d <= 3) {
       Bins bins;
-      double* bx = ensure<double>(ctx->bx, (size_t)ns);
-      double* by = ensure<double>(ctx->by, (size_t)ns);
-      double* bz = ensure<double>(ctx->bz, (size_t)ns);
+      double* bx = ensure<double>(ctx->bx, (size_t)ns * 3);
+      double* by = bx + ns;
+      double* bz = bx + 2 * ns;
       double* bt = ensure<double>(ctx->bt, (size_t)ns);
       int* bidx = ensure<int>(ctx->bidx, (size_t)ns);
       int* cs = ensure<int>(ctx->cell_start, (size_t)g.n_cells + 1);
@@ -1187,6 +1200,7 @@ int vx_prune(vx_context* ctx_in, const vx_problem* P, uint8_t* dropped_out, int6
       const size_t cub_bytes = bin_tmp_bytes(ns, g.n_cells);
       void* cub = ensure<char>(ctx->cub, cub_bytes);
       bins.x = bx; bins.y = by; bins.z = bz; bins.t = bt; bins.idx = bidx; bins.cell_start = cs;
+      bins.stride = ns;
       bins.f4 = nullptr;
       bin_checked(g, p3, tdev, nullptr, cub, cub_bytes, ka, kb, va, vb, bx, by, bz, bt, bidx,
                   (float4*)nullptr, cs, prm, ctr, st);
