@@ -701,17 +701,6 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
     }
     Geo g;
     fill_geo(g, P, zb, ze, ns, xy2d);
-    if (!use_brute) {  // exact voxel centres per axis (<= 4 Mi entries; else computed inline)
-      const long long tot = g.n[0] + g.n[1] + g.n[2];
-      if (tot <= (4ll << 20)) {
-        g.ctab_off[0] = 0;
-        g.ctab_off[1] = g.n[0];
-        g.ctab_off[2] = g.n[0] + g.n[1];
-        double* ct = ensure<double>(ctx->ctab, (size_t)tot);
-        g.ctab = ct;
-        launches += launch_centres(g, ct, st);
-      }
-    }
     int32_t* lab = host_io ? ensure<int32_t>(ctx->labels, (size_t)nvs) : labels_out;
     double* dist = nullptr;
     // host-buffer call into pageable memory: stage through pinned buffers

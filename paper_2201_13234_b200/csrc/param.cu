@@ -180,19 +180,6 @@ int launch_params(const Geo& g, const Bins& bins, DevParams* prm, const DevCount
   return n;
 }
 
-__global__ void centres_kernel(Geo g, double* ctab, long long total) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  const int a = i >= g.ctab_off[2] ? 2 : (i >= g.ctab_off[1] ? 1 : 0);
-  ctab[i] = center(i - g.ctab_off[a], g.sp[a]);  // geometry.hpp:58-60
-}
-
-int launch_centres(const Geo& g, double* ctab, cudaStream_t st) {
-  const long long total = g.ctab_off[2] + g.n[2];
-  centres_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(g, ctab, total);
-  return 1;
-}
-
 int launch_init(DevParams* prm, DevCounters* ctr, cudaStream_t st) {
   init_kernel<<<1, 1, 0, st>>>(prm, ctr);
   return 1;
