@@ -79,7 +79,7 @@ struct vx_context {
   std::mutex mu;
   Buf pos_raw, t_raw, w_raw, p3, t, dropped, keys_a, keys_b, vals_a, vals_b, bx, by, bz, bt, bidx,
       cell_start, cub, labels, dist, hist, unres, params, counters, scratch, vsample, vlab, vdist,
-      vbad, slots, f4, sb_info, sb_list, sb_count, sb_slots, sb_ovf, ctab;
+      vbad, slots, f4, sb_info, sb_list, sb_count, sb_slots, sb_ovf, ctab, nd_x, nd_t, nd_idx, nd_cells;
   DevParams* h_prm = nullptr;
   DevCounters* h_ctr = nullptr;
   cudaEvent_t ev[8] = {};  // stage markers (options.profile_stages)
@@ -98,11 +98,11 @@ struct vx_context {
   // default contexts when their thread exits, and a failed create_context.
   ~vx_context();
 
-  Buf* all[36] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
+  Buf* all[40] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
                   &vals_a,  &vals_b,  &bx,    &by,    &bz,     &bt,      &bidx,     &cell_start,
                   &cub,     &labels,  &dist,  &hist,  &unres,  &params,  &counters, &scratch,
                   &vsample, &vlab,    &vdist, &vbad,  &slots,  &f4,      &sb_info,  &sb_list,
-                  &sb_count, &sb_slots, &sb_ovf, &ctab};
+                  &sb_count, &sb_slots, &sb_ovf, &ctab, &nd_x,  &nd_t,   &nd_idx,   &nd_cells};
 };
 
 namespace {
@@ -615,13 +615,16 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
   // a whole 2-D image: (x, y) embedding, one "plane" of n0 n1 voxels
   // (embedded y rides in gridDim.y of the ball kernels: <= 65535 super-brick
   // rows); a whole 1-D image likewise maps to embedded x
-  const bool xy2d = (d == 2 || d == 1) && !brute_engine && zb == 0 && ze == n_last &&
+  // d != 3: the d-dimensional engine (ballnd.cu); VX_ND_OFF=1 keeps the
+  // older routes (d = 1, 2 embedded into the 3-D kernels, d >= 4 brute force)
+  const bool use_nd = !brute_engine && d != 3 && !std::getenv("VX_ND_OFF");
+  const bool xy2d = !use_nd && (d == 2 || d == 1) && !brute_engine && zb == 0 && ze == n_last &&
                     (d == 1 || n_last <= 1000000) && !std::getenv("VX_2D_XZ");
   if (O.asynchronous && !O.device_pointers)
     return fail(VX_EINVAL, "asynchronous calls need device pointers");
   const bool host_io = !O.device_pointers;
   const bool do_prune = !brute_engine && timed(P) && O.prune;
-  const bool use_brute = brute_engine || d > 3;
+  const bool use_brute = brute_engine || (d > 3 && !use_nd);
   double t_min_host = std::numeric_limits<double>::quiet_NaN();
   // Host buffers: the positions are validated on the device during ingest
   // (the same predicate, sites.cpp:54-57) and the call fails right after it,
@@ -726,7 +729,9 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
     const bool p3_alias = !use_brute && d == 3 && g.emb[0] == 0 && g.emb[1] == 1 && g.emb[2] == 2;
     const bool t_alias = timed(P) && times != nullptr;
     double* t_copy = timed(P) && !t_alias ? ensure<double>(ctx->t, (size_t)ns) : nullptr;
-    double* p3_copy = use_brute || p3_alias ? nullptr : ensure<double>(ctx->p3, (size_t)ns * 3);
+    // the embedded 3-D copy of the 3-D engine
+    const bool want_p3 = !use_brute && !p3_alias && !use_nd;
+    double* p3_copy = want_p3 ? ensure<double>(ctx->p3, (size_t)ns * 3) : nullptr;
     const double* tdev = t_alias ? times : t_copy;
     const double* p3 = p3_alias ? pos : p3_copy;
     Len16 len;
@@ -744,7 +749,57 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
     tm.mark(1);
 
     double r0 = std::numeric_limits<double>::quiet_NaN();
-    if (use_brute) {
+    if (use_nd) {
+      unsigned* ka = ensure<unsigned>(ctx->keys_a, (size_t)ns);
+      unsigned* kb = ensure<unsigned>(ctx->keys_b, (size_t)ns);
+      int* va = ensure<int>(ctx->vals_a, (size_t)ns);
+      int* vb = ensure<int>(ctx->vals_b, (size_t)ns);
+      GeoN gn;
+      fill_geo_nd(gn, P->kind, d, P->periodic, reinterpret_cast<const long long*>(P->counts), P->lengths, g.growth,
+                  ns, zb, ze);
+      const size_t cub_bytes = bin_tmp_bytes(ns, std::max<long long>(gn.n_cells, g.n_cells));
+      void* cub = ensure<char>(ctx->cub, cub_bytes);
+      uint8_t* dropped = nullptr;
+      double* nx = ensure<double>(ctx->nd_x, (size_t)ns * d);
+      double* nt = timed(P) ? ensure<double>(ctx->nd_t, (size_t)ns) : nullptr;
+      int* nidx = ensure<int>(ctx->nd_idx, (size_t)ns);
+      int* ncs = ensure<int>(ctx->nd_cells, (size_t)gn.n_cells + 1);
+      const BinsN bins{nx, ns, nt, nidx, ncs};
+      if (do_prune) {  // bin every site, prune against the cells, re-bin the survivors
+        dropped = ensure<uint8_t>(ctx->dropped, (size_t)ns);
+        const int nb0 = launch_bin_nd(gn, pos, tdev, nullptr, cub, cub_bytes, ka, kb, va, vb, nx, nt, nidx, ncs, prm,
+                                      ctr, st);
+        if (nb0 < 0) ck(static_cast<cudaError_t>(-1000 - nb0), "radix sort");
+        launches += nb0;
+        launches += launch_prune_nd(gn, bins, pos, tdev, prm, dropped, st);
+        dbg(st, "prune");
+      }
+      const int nbin = launch_bin_nd(gn, pos, tdev, dropped, cub, cub_bytes, ka, kb, va, vb, nx, nt, nidx, ncs, prm,
+                                     ctr, st);
+      if (nbin < 0) ck(static_cast<cudaError_t>(-1000 - nbin), "radix sort");
+      launches += nbin;
+      dbg(st, "bin");
+      tm.mark(2);
+      if (!timed(P)) r0 = ns == 1 ? cover_radius(d, P->lengths, P->periodic) : optimal_r0(ns, d, P->lengths);
+      Bins bt;
+      std::memset(&bt, 0, sizeof(bt));
+      bt.t = nt;
+      Geo gp = g;  // the cost model reads kind, dim, growth, volume, lengths
+      gp.lmax = gn.lmax;
+      double* scratch = ensure<double>(ctx->scratch, 1024);
+      launches += launch_params(gp, bt, prm, ctr, O.has_override, O.override_param, r0, ball_scale, scratch, st);
+      dbg(st, "params");
+      tm.mark(3);
+      const long long cap = (long long)std::min<int64_t>(nvs, 1ll << 26);
+      long long* unres = ensure<long long>(ctx->unres, (size_t)cap);
+      launches += launch_ball_nd(gn, bins, prm, lab, dist, hist, unres, cap, ctr, nvs, st);
+      dbg(st, "ball nd");
+      tm.mark(4);
+      launches += launch_unres_nd(gn, bins, prm, unres, cap, lab, dist, hist, ctr, nvs, st);
+      dbg(st, "unresolved nd");
+      tm.mark(5);
+      if (sink) sink_chunks.push_back({zb, ze, sink_event(ctx, 0, st)});
+    } else if (use_brute) {
       uint8_t* dropped = nullptr;
       if (do_prune) {
         dropped = ensure<uint8_t>(ctx->dropped, (size_t)ns);

@@ -297,7 +297,8 @@ def test_device_pointer_path_matches_host(oracle_mod):
     eng.close()
 
 
-def test_high_dimension_uses_brute_engine(oracle_mod):
+def test_high_dimension_uses_the_fast_engine(oracle_mod):
+    """d >= 4 runs the d-dimensional gather engine (ballnd.cu), not brute force."""
     rng = np.random.default_rng(5)
     for kind in (0, 1, 2):
         pos, t = oracle_mod.generate_uniform_sites(4, np.array([1.0, 0.7, 1.3, 0.9]), 23, kind, 0.7,
@@ -305,8 +306,70 @@ def test_high_dimension_uses_brute_engine(oracle_mod):
         p = oracle_mod.Problem(kind, [5, 4, 6, 3], [1.0, 0.7, 1.3, 0.9], kind != 1, pos, t, 1.3)
         lab, dist = oracle_mod.brute(p)
         r = run_fast(p, prune=False)
-        assert r.stats["engine"] == 1
+        assert r.stats["engine"] == 0
         assert np.array_equal(r.labels.labels, lab) and np.array_equal(bits(r.distances.values), bits(dist))
+
+
+@pytest.mark.parametrize("d", [1, 2, 4, 5, 6, 7, 9])
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_nd_engine_vs_reference(d, kind):
+    """The d != 3 engine against the reference library (oracle/_ref) on random
+    instances: both boundaries, prune on/off, an override parameter, densities
+    from ~1.5 to ~15 voxels per site per axis, anisotropic lengths; labels, f64
+    distances and histogram bit for bit."""
+    import oracle
+    import paper_2201_13234_b200 as vx
+
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(100 * d + kind)
+    tgt = {1: 40000, 2: 90000, 4: 90000, 5: 60000, 6: 60000, 7: 30000, 9: 20000}[d]
+    for it in range(4):
+        L = rng.uniform(0.5, 2.0, d)
+        counts = [max(1, int(tgt ** (1.0 / d) * np.exp(rng.uniform(-0.4, 0.4)))) for _ in range(d)]
+        nv = int(np.prod(counts))
+        spacing = float(np.exp(rng.uniform(np.log(1.5), np.log(15.0))))
+        ns = int(np.clip(nv / spacing ** d, 1, 4000))
+        horizon = float(0.5 * np.prod(L) ** (1.0 / d) / ns ** (1.0 / d))
+        pos, t = oracle.generate_uniform_sites(d, L, ns, kind, horizon, int(rng.integers(1 << 40)))
+        G = [0.0, float(np.exp(rng.uniform(-1, 1))), float(np.exp(rng.uniform(-1, 1)))][kind]
+        p = oracle.Problem(kind, counts, L, it % 2 == 0, pos, t, G)
+        prune = it != 1
+        override = None
+        if it == 3:
+            _, _, param, _ = oracle.ref_tessellate(p, prune=prune, distances=False)
+            override = param * 0.7 if kind == 0 else float(np.min(t) + 0.7 * (param - np.min(t)))
+        lab, dist, _, _ = oracle.ref_tessellate(p, prune=prune, override=override)
+        sites, grid = to_vx(p)
+        r = vx.tessellate_fast(sites, grid, vx.FastOptions(override_param=override, prune=prune), distances=True,
+                               histogram=True)
+        assert r.stats["engine"] == 0
+        assert np.array_equal(r.labels.labels, lab), (it, int((r.labels.labels != lab).sum()))
+        assert np.array_equal(bits(r.distances.values), bits(dist)), it
+        assert np.array_equal(r.histogram, np.bincount(lab, minlength=ns).astype(np.uint64)), it
+
+
+@pytest.mark.parametrize("d", [1, 2, 4])
+def test_nd_slabs_concatenate_to_the_whole_image(oracle_mod, d):
+    """Slabs of the last axis through the d != 3 engine (the multi-GPU
+    decomposition): concatenated, they equal the whole image; histograms add."""
+    import paper_2201_13234_b200 as vx
+
+    rng = np.random.default_rng(7 + d)
+    counts = {1: [3000], 2: [90, 77], 4: [9, 8, 10, 11]}[d]
+    L = rng.uniform(0.6, 1.6, d)
+    pos, t = oracle_mod.generate_uniform_sites(d, L, 300, 1, 0.05, 17)
+    p = oracle_mod.Problem(1, counts, L, True, pos, t, 1.1)
+    lab, _ = oracle_mod.brute(p, distances=False)
+    sites, grid = to_vx(p)
+    n = counts[-1]
+    parts, hist = [], np.zeros(300, dtype=np.uint64)
+    for a, b in ((0, n // 3), (n // 3, n // 3 + 1), (n // 3 + 1, n)):
+        r = vx.tessellate_fast(sites, grid, distances=False, histogram=True, slab=(a, b))
+        parts.append(np.asarray(r.labels.labels))
+        hist += r.histogram
+    assert np.array_equal(np.concatenate(parts), lab)
+    assert np.array_equal(hist, np.bincount(lab, minlength=300).astype(np.uint64))
 
 
 @pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
