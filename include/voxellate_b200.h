@@ -20,7 +20,16 @@
  *    (same message text), VX_ECUDA/VX_ENOMEM for device failures.
  *  - every call blocks unless vx_options.asynchronous is set; inputs are read
  *    only, outputs are caller-allocated.  Calls on distinct contexts may run
- *    concurrently.
+ *    concurrently.  Calls on ONE context share its device workspaces: they
+ *    are serialized on the host (a mutex) and on the device (a call on a
+ *    different stream than the context's previous call first waits for that
+ *    stream), so asynchronous calls on one context never overlap; a CUDA
+ *    graph captured from a context must not be replayed concurrently with
+ *    other work on that context.
+ *  - TessResult.param / EvalCounters of the C++ shim are this engine's: the
+ *    r0 is the reference's bit for bit, the timed t0 is this engine's own
+ *    device cost scan (labels never depend on it), and the counters count
+ *    this engine's ball-phase / unresolved-phase exact evaluations.
  */
 #ifndef VOXELLATE_B200_H
 #define VOXELLATE_B200_H

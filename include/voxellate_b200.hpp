@@ -5,6 +5,8 @@
 //   voxellate::prune_ineffective_sites              (include/voxellate/sites.hpp:69)
 //   voxellate::validate_partition                   (include/voxellate/tessellate.hpp:81-84)
 //   voxellate::generate_uniform_sites               (include/voxellate/sites.hpp:48-49)
+//   voxellate::spheres_to_timed_sites               (include/voxellate/sites.hpp:52)
+//   voxellate::scan_ball / ball_voxels              (include/voxellate/tessellate.hpp:62-68)
 // and value types with the same fields (Domain, VoxelGrid, SiteSet, FastOptions,
 // TessResult, ...), in namespace vxb200 so it can coexist with the reference in
 // one program.  Errors become the reference's exceptions: VX_EINVAL ->
@@ -14,6 +16,7 @@
 //     namespace voxellate = vxb200;   // and link libvoxellate_b200.so
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <limits>
@@ -103,6 +106,16 @@ struct DistanceImage {
   VoxelGrid grid;
   std::vector<double> values;
 };
+// Boundary note -- two TessResult fields report THIS engine's numbers, not
+// the reference's (labels and distances never depend on them):
+//  * counters: step1_evals = exact evaluations of the ball phase (per voxel,
+//    the candidates of its octant / sub-brick list), step2_evals = those of
+//    the unresolved-voxel search; the reference counts its window scan and
+//    all-sites step 2 (tessellate.cpp:264-270);
+//  * param: for Voronoi the reference's r0 bit for bit; for the timed kinds
+//    the t0 this engine's device cost scan chose (the reference reports its
+//    golden-section search_optimal_t0, cost.cpp:98-146).  An explicit
+//    FastOptions::override_param is used and reported as given by both.
 struct EvalCounters {  // this engine's counts: ball phase / shell phase evaluations
   std::uint64_t step1_evals = 0;
   std::uint64_t step2_evals = 0;
@@ -118,6 +131,12 @@ struct FastOptions {
   std::optional<double> override_param;
   bool prune = true;
   int n_gpus = 1;  // extension: split the call over this many devices
+};
+struct LaguerreSpheres {  // sites.hpp:34-45
+  int dim = 0;
+  std::vector<double> positions;  // count() * dim
+  std::vector<double> radii;
+  std::int64_t count() const { return dim == 0 ? 0 : (std::int64_t)positions.size() / dim; }
 };
 struct PruneResult {
   SiteSet sites;
@@ -236,6 +255,113 @@ inline ValidationReport validate_partition(const LabelImage& labels, const Dista
 }
 
 // sites.hpp:48-49
+// t_s = -(r_s * r_s) / G, same checks and messages as sites.cpp:87-104
+inline SiteSet spheres_to_timed_sites(const LaguerreSpheres& spheres, double growth) {
+  if (!(growth > 0.0)) throw std::invalid_argument("growth rate G must be positive");
+  if (spheres.count() < 1) throw std::invalid_argument("sphere set must contain at least one sphere");
+  if ((std::int64_t)spheres.radii.size() != spheres.count())
+    throw std::invalid_argument("sphere set must carry one radius per center");
+  SiteSet out;
+  out.kind = Kind::Laguerre;
+  out.dim = spheres.dim;
+  out.growth = growth;
+  out.positions = spheres.positions;
+  out.times.reserve(spheres.radii.size());
+  for (double r : spheres.radii) {
+    if (!(r >= 0.0)) throw std::invalid_argument("sphere radii must be nonnegative");
+    out.times.push_back(-(r * r) / growth);
+  }
+  return out;
+}
+
+using Point = std::vector<double>;
+
+// Visits every voxel whose centre lies within `radius` of `center`, once
+// (tessellate.hpp:62-68): per axis the candidate indices of a conservative
+// window ((c -/+ r(1 + 1e-9)) / h - 0.5, rounded outwards with a relative
+// slack) and their squared residuals (periodic: wrapped), then an odometer
+// over the axes -- last axis outermost, axis 0 innermost, i.e. ascending
+// window order -- accumulating the squared terms from the last axis down to
+// axis 0 (the reference's fold, geometry.hpp:106-123) and pruning partial
+// sums beyond the inflated radius; a voxel is visited iff dsq <= radius^2.
+// Host code: this is the reference's investigation-ball enumeration, not a
+// step of the GPU pipeline (which gathers per voxel block instead).
+template <class Visit>
+inline void scan_ball(const Point& center, double radius, const VoxelGrid& grid, Visit&& visit) {
+  const int d = grid.dim();
+  if ((int)center.size() != d) throw std::invalid_argument("ball center dimension does not match the grid");
+  if (!(std::isfinite(radius) && radius >= 0.0)) throw std::invalid_argument("ball radius must be nonnegative");
+  const double rp = radius * (1.0 + 1e-9), r2p = rp * rp, r2 = radius * radius;
+  const bool per = grid.domain.periodic();
+  std::vector<std::vector<std::int64_t>> idx(d);
+  std::vector<std::vector<double>> sq(d);
+  std::vector<std::int64_t> stride(d);
+  std::int64_t st = 1;
+  for (int a = 0; a < d; ++a) {
+    stride[a] = st;
+    st *= grid.counts[a];
+    const std::int64_t n = grid.counts[a];
+    const double h = grid.spacing[a], L = grid.domain.lengths[a], iL = grid.domain.inv_lengths[a];
+    const double lo_t = (center[a] - rp) / h - 0.5, hi_t = (center[a] + rp) / h - 0.5;
+    const double slack = 1e-9 * (std::fabs(lo_t) + std::fabs(hi_t) + 1.0);
+    const double klo = std::ceil(lo_t - slack), khi = std::floor(hi_t + slack);
+    if (khi < klo) return;
+    // separately rounded products (volatile: no FMA contraction whatever the
+    // caller's compiler flags), as the reference build computes them
+    auto mul = [](double x, double y) {
+      volatile double r = x * y;
+      return (double)r;
+    };
+    auto add = [&](std::int64_t k) {
+      double w = center[a] - mul((double)k + 0.5, h);                      // geometry.hpp:58-60
+      if (per) w = w - mul(std::floor(mul(w, iL) + 0.5), L);                // geometry.hpp:80-89
+      idx[a].push_back(k);
+      sq[a].push_back(mul(w, w));
+    };
+    if (per) {
+      if (khi - klo + 1.0 >= (double)n) {
+        for (std::int64_t k = 0; k < n; ++k) add(k);
+      } else {
+        for (std::int64_t k = (std::int64_t)klo; k <= (std::int64_t)khi; ++k) add(((k % n) + n) % n);
+      }
+    } else {
+      const std::int64_t a0 = klo <= 0.0 ? 0 : (std::int64_t)std::min(klo, (double)n);
+      const std::int64_t a1 = khi >= (double)(n - 1) ? n - 1 : (std::int64_t)std::max(khi, -1.0);
+      for (std::int64_t k = a0; k <= a1; ++k) add(k);
+    }
+    if (idx[a].empty()) return;
+  }
+  // odometer: pos[a] walks idx[a]; acc[a] = sum of the terms of axes >= a
+  std::vector<std::size_t> pos(d, 0);
+  std::vector<double> acc(d + 1, 0.0);
+  std::vector<std::int64_t> lin(d + 1, 0);
+  int a = d - 1;
+  while (true) {
+    if (pos[a] < idx[a].size()) {
+      const double s = acc[a + 1] + sq[a][pos[a]];
+      const std::int64_t l = lin[a + 1] + idx[a][pos[a]] * stride[a];
+      ++pos[a];
+      if (!(s <= r2p)) continue;
+      if (a == 0) {
+        if (s <= r2) visit(l);
+      } else {
+        acc[a] = s;
+        lin[a] = l;
+        --a;
+        pos[a] = 0;
+      }
+    } else {
+      if (++a == d) return;
+    }
+  }
+}
+
+inline std::vector<std::int64_t> ball_voxels(const Point& center, double radius, const VoxelGrid& grid) {
+  std::vector<std::int64_t> out;
+  scan_ball(center, radius, grid, [&](std::int64_t l) { out.push_back(l); });
+  return out;
+}
+
 inline SiteSet generate_uniform_sites(const Domain& domain, std::int64_t n_sites, Kind kind,
                                       double growth, double time_horizon, std::uint64_t seed) {
   SiteSet s;

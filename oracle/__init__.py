@@ -96,6 +96,8 @@ def ref():
                                                _P, _P, _I64, C.c_uint64, _P]
         L.vxref_tessellate_timed.argtypes = [C.c_int, C.c_int, C.c_int, _P, _P, _I64, _P, _P, _D,
                                              C.c_int, _P, _P, _P, _P]
+        L.vxref_ball_voxels.argtypes = [C.c_int, C.c_int, _P, _P, _P, _D, _P, _I64]
+        L.vxref_ball_voxels.restype = _I64
         L.vxref_max_threads.restype = C.c_int
         L.vxref_have_image_io.restype = C.c_int
         if L.vxref_have_image_io():
@@ -246,6 +248,20 @@ def ref_tessellate_timed(p: Problem, threads=0, labels=False):
     if rc:
         raise (ValueError if rc == 1 else RuntimeError)(ref().vxref_last_error().decode())
     return float(sec[0]), "%016x" % int(fp[0]), float(param[0]), lab
+
+
+def ref_ball_voxels(counts, lengths, periodic, center, radius):
+    """The reference's ball_voxels (tessellate.hpp:66-68), in visit order."""
+    counts = np.ascontiguousarray(counts, dtype=np.int64)
+    lengths = np.ascontiguousarray(lengths, dtype=np.float64)
+    center = np.ascontiguousarray(center, dtype=np.float64)
+    cap = int(np.prod(counts))
+    out = np.empty(cap, dtype=np.int64)
+    n = ref().vxref_ball_voxels(counts.size, int(periodic), _ptr(counts), _ptr(lengths), _ptr(center),
+                                float(radius), _ptr(out), cap)
+    if n < 0:
+        raise ValueError(ref().vxref_last_error().decode())
+    return out[:n]
 
 
 def ref_spheres_to_timed(positions, radii, growth, dim=3):

@@ -148,6 +148,20 @@ int vxref_tessellate_timed(int kind, int dim, int periodic, const int64_t* count
   });
 }
 
+// scan_ball / ball_voxels (tessellate.hpp:62-68): writes up to cap voxel
+// indices in visit order; returns the count (>= 0) or -1 on error.
+int64_t vxref_ball_voxels(int dim, int periodic, const int64_t* counts, const double* lengths,
+                          const double* center, double radius, int64_t* out, int64_t cap) {
+  int64_t n = -1;
+  guarded([&] {
+    const VoxelGrid grid = make_grid(dim, periodic, counts, lengths);
+    const std::vector<int64_t> v = ball_voxels(Point(center, center + dim), radius, grid);
+    for (size_t i = 0; i < v.size() && (int64_t)i < cap; ++i) out[i] = v[i];
+    n = (int64_t)v.size();
+  });
+  return n;
+}
+
 // Returns the number of removed sites (>= 0) or -1 on error; dropped_out[s]=1
 // for removed sites.
 int64_t vxref_prune(int kind, int dim, int periodic, const double* lengths, int64_t n_sites,

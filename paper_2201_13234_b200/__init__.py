@@ -9,8 +9,8 @@ package only binds it.  There is no CPU fallback.
 from ._lib import LIB_PATH, VxError, lib  # noqa: F401
 from .voxellate import (  # noqa: F401
     Boundary, DistanceImage, Domain, EvalCounters, FastOptions, ImageMeta, Kind, LabelImage,
-    LaguerreSpheres, PruneResult, SiteSet, TessResult, ValidationReport, VoxelGrid,
-    generate_uniform_sites, optimal_r0, prune_ineffective_sites, read_distance_image,
+    LaguerreSpheres, PruneResult, SiteSet, TessResult, ValidationReport, VoxelGrid, ball_voxels,
+    generate_uniform_sites, scan_ball, optimal_r0, prune_ineffective_sites, read_distance_image,
     read_label_image, slab_bounds, spheres_to_timed_sites, tessellate_brute, tessellate_fast,
     tessellate_to_files, validate_partition, write_distance_image, write_label_image)
 
@@ -19,5 +19,5 @@ __all__ = [
     "tessellate_fast", "tessellate_brute", "prune_ineffective_sites", "validate_partition",
     "generate_uniform_sites", "spheres_to_timed_sites", "optimal_r0", "slab_bounds",
     "ImageMeta", "write_label_image", "write_distance_image", "read_label_image",
-    "read_distance_image", "tessellate_to_files",
+    "read_distance_image", "tessellate_to_files", "ball_voxels", "scan_ball", "LaguerreSpheres",
 ]

@@ -85,6 +85,8 @@ struct vx_context {
   cudaEvent_t ev[8] = {};  // stage markers (options.profile_stages)
   bool ev_marked[8] = {};  // which markers the last profiled call recorded
   cudaStream_t copy_stream = nullptr;  // chunked D2H of host-buffer calls
+  cudaStream_t last_stream = nullptr;  // the stream of the context's previous call
+  cudaEvent_t handoff_ev = nullptr;    // orders a call after the previous one on another stream
   cudaEvent_t chunk_ev[16] = {};
   std::vector<cudaEvent_t> sink_ev;    // vx_tessellate_to_files: one per chunk
   cudaEvent_t done_ev[2] = {};
@@ -152,6 +154,7 @@ vx_context::~vx_context() {
     if (b) cudaFreeHost(b);
   for (auto e : ev)
     if (e) cudaEventDestroy(e);
+  if (handoff_ev) cudaEventDestroy(handoff_ev);
   cudaGetLastError();
 }
 
@@ -659,6 +662,22 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
   std::lock_guard<std::mutex> lock(ctx->mu);
   DeviceGuard guard(ctx->device);
   cudaStream_t st = O.stream ? static_cast<cudaStream_t>(O.stream) : ctx->stream;
+  {
+    // Calls on one context share its workspaces (bins, lists, counters): a
+    // call on another stream than the previous one first waits for that
+    // stream, so asynchronous calls on one context never overlap.  (Inside a
+    // stream capture the caller orders the replays.)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusNone && ctx->last_stream && ctx->last_stream != st) {
+      if (!ctx->handoff_ev && cudaEventCreateWithFlags(&ctx->handoff_ev, cudaEventDisableTiming) != cudaSuccess)
+        return fail(VX_ECUDA, "context handoff event: " + std::string(cudaGetErrorString(cudaGetLastError())));
+      if (cudaEventRecord(ctx->handoff_ev, ctx->last_stream) != cudaSuccess ||
+          cudaStreamWaitEvent(st, ctx->handoff_ev, 0) != cudaSuccess)
+        cudaGetLastError();  // the previous stream was destroyed: nothing left to wait for
+    }
+    if (cs == cudaStreamCaptureStatusNone) ctx->last_stream = st;
+  }
   int launches = 0;
   int64_t plane = 1;
   for (int i = 0; i < d - 1; ++i) plane *= P->counts[i];

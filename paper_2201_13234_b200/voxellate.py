@@ -369,6 +369,66 @@ def spheres_to_timed_sites(spheres: LaguerreSpheres, growth: float) -> SiteSet:
     return SiteSet(Kind.Laguerre, spheres.dim, spheres.positions, -(r * r) / growth, float(growth))
 
 
+def ball_voxels(center: Sequence[float], radius: float, grid: VoxelGrid) -> np.ndarray:
+    """Every voxel whose centre lies within ``radius`` of ``center``, once, in
+    the reference's visit order (tessellate.hpp:62-68): per axis the indices of
+    a conservative window ((c -/+ r (1 + 1e-9)) / h - 0.5 rounded outwards with
+    a relative slack; periodic windows wrap, one spanning the whole axis lists
+    each index once) with their squared (periodic: wrapped) residuals, folded
+    from the last axis to axis 0 (geometry.hpp:106-123); the last axis varies
+    slowest.  A voxel is kept iff dsq <= radius^2.  numpy evaluates each
+    operation separately rounded, like the reference build."""
+    d = grid.dim()
+    center = np.asarray(center, dtype=np.float64)
+    if center.size != d:
+        raise ValueError("ball center dimension does not match the grid")
+    radius = float(radius)
+    if not (np.isfinite(radius) and radius >= 0.0):
+        raise ValueError("ball radius must be nonnegative")
+    rp = radius * (1.0 + 1e-9)
+    per = grid.domain.periodic()
+    idx, sq, stride = [], [], []
+    st = 1
+    for a in range(d):
+        n = int(grid.counts[a])
+        stride.append(st)
+        st *= n
+        h = grid.spacing[a] if hasattr(grid, "spacing") else grid.domain.lengths[a] / n
+        L = float(grid.domain.lengths[a])
+        lo_t = (center[a] - rp) / h - 0.5
+        hi_t = (center[a] + rp) / h - 0.5
+        slack = 1e-9 * (abs(lo_t) + abs(hi_t) + 1.0)
+        klo, khi = np.ceil(lo_t - slack), np.floor(hi_t + slack)
+        if khi < klo:
+            return np.empty(0, dtype=np.int64)
+        if per:
+            ks = np.arange(n) if khi - klo + 1.0 >= n else np.mod(np.arange(int(klo), int(khi) + 1), n)
+        else:
+            a0 = 0 if klo <= 0.0 else int(min(klo, float(n)))
+            a1 = n - 1 if khi >= float(n - 1) else int(max(khi, -1.0))
+            ks = np.arange(a0, a1 + 1)
+        if ks.size == 0:
+            return np.empty(0, dtype=np.int64)
+        w = center[a] - (ks.astype(np.float64) + 0.5) * h
+        if per:
+            w = w - np.floor(w * grid.domain.inv_lengths[a] + 0.5) * L
+        idx.append(ks.astype(np.int64))
+        sq.append(w * w)
+    acc, lin = sq[d - 1], idx[d - 1] * stride[d - 1]
+    for a in range(d - 2, -1, -1):
+        acc = np.add.outer(acc, sq[a])
+        lin = np.add.outer(lin, idx[a] * stride[a])
+    acc, lin = acc.reshape(-1), lin.reshape(-1)
+    return lin[acc <= radius * radius].astype(np.int64)
+
+
+def scan_ball(center: Sequence[float], radius: float, grid: VoxelGrid, visit) -> None:
+    """tessellate.hpp:62-65: calls visit(linear_index) for every voxel of
+    ball_voxels(center, radius, grid), in the same order."""
+    for v in ball_voxels(center, radius, grid):
+        visit(int(v))
+
+
 def optimal_r0(n_sites: int, domain: Domain) -> float:
     """radius_from_volume(optimal_v0(N_s, V), d) (cost.cpp:28-39)."""
     out = C.c_double(0.0)

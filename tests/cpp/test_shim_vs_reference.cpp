@@ -176,6 +176,64 @@ int main() {
     }
   }
 #endif
+  {  // ball_voxels / scan_ball (tessellate.hpp:62-68), spheres_to_timed_sites (sites.hpp:52)
+    std::mt19937_64 e2(77);
+    for (int it = 0; it < 200; ++it) {
+      const int d = 1 + it % 4;
+      const bool per = it % 2;
+      std::vector<double> L(d), c(d);
+      std::vector<std::int64_t> counts(d);
+      for (int a = 0; a < d; ++a) {
+        L[a] = uni(e2, 0.5, 2.0);
+        counts[a] = 1 + (std::int64_t)(e2() % (d == 1 ? 300 : (d == 2 ? 60 : (d == 3 ? 20 : 10))));
+        c[a] = uni(e2, -0.2, 1.2) * L[a];
+      }
+      double diag = 0.0;
+      for (double x : L) diag += x * x;
+      double r = uni(e2, 0.0, 1.2) * std::sqrt(diag);
+      R::VoxelGrid rg(counts, R::Domain(L, per ? R::Boundary::Periodic : R::Boundary::NonPeriodic));
+      G::VoxelGrid gg(counts, G::Domain(L, per ? G::Boundary::Periodic : G::Boundary::NonPeriodic));
+      if (it % 5 == 0) {  // a voxel centre exactly on the sphere
+        double s2 = 0.0;
+        for (int a = 0; a < d; ++a) {
+          const double x = rg.center_coord(a, (std::int64_t)(e2() % counts[a]));
+          s2 += (c[a] - x) * (c[a] - x);
+        }
+        r = std::sqrt(s2);
+      }
+      CHECK(G::ball_voxels(c, r, gg) == R::ball_voxels(c, r, rg));
+      std::int64_t visits = 0;
+      G::scan_ball(c, r, gg, [&](std::int64_t) { ++visits; });
+      CHECK(visits == (std::int64_t)R::ball_voxels(c, r, rg).size());
+    }
+    bool t1 = false, t2 = false;
+    try { G::ball_voxels({0.5}, -1.0, G::VoxelGrid({4}, G::Domain({1.0}, G::Boundary::Periodic))); }
+    catch (const std::invalid_argument& e) { t1 = std::string(e.what()) == "ball radius must be nonnegative"; }
+    try { G::ball_voxels({0.5, 0.5}, 0.1, G::VoxelGrid({4}, G::Domain({1.0}, G::Boundary::Periodic))); }
+    catch (const std::invalid_argument& e) { t2 = std::string(e.what()) == "ball center dimension does not match the grid"; }
+    CHECK(t1 && t2);
+    R::LaguerreSpheres rs;
+    G::LaguerreSpheres gs;
+    rs.dim = gs.dim = 3;
+    for (int i = 0; i < 30; ++i) {
+      for (int a = 0; a < 3; ++a) {
+        const double x = uni(e2, 0.01, 0.99);
+        rs.positions.push_back(x);
+        gs.positions.push_back(x);
+      }
+      const double rad = uni(e2, 0.0, 0.2);
+      rs.radii.push_back(rad);
+      gs.radii.push_back(rad);
+    }
+    const R::SiteSet a = R::spheres_to_timed_sites(rs, 1.7);
+    const G::SiteSet b = G::spheres_to_timed_sites(gs, 1.7);
+    CHECK(a.times == b.times && a.positions == b.positions && b.kind == G::Kind::Laguerre && b.growth == 1.7);
+    gs.radii[3] = -1.0;
+    bool t3 = false;
+    try { G::spheres_to_timed_sites(gs, 1.0); }
+    catch (const std::invalid_argument& e) { t3 = std::string(e.what()) == "sphere radii must be nonnegative"; }
+    CHECK(t3);
+  }
   std::printf("%d instances, %d failures\n", instances, failures);
   if (failures == 0) std::printf("ALL OK\n");
   return failures == 0 ? 0 : 1;

@@ -79,3 +79,37 @@ def test_voxel_grid_order_axis0_fastest():
     assert g.linear_index([1, 2, 3]) == 1 + 3 * (2 + 4 * 3)
     assert g.decompose(1 + 3 * (2 + 4 * 3)) == [1, 2, 3]
     assert g.center_coord(1, 2) == (2 + 0.5) * 0.25
+
+
+def test_ball_voxels_matches_reference():
+    """ball_voxels / scan_ball (tessellate.hpp:62-68): the same voxels in the
+    same visit order as the reference library, on random grids (d = 1..4,
+    both boundaries), centres anywhere in the domain, radii from 0 to past the
+    domain size, and exact-boundary radii (a voxel centre at distance r)."""
+    import oracle
+
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    import paper_2201_13234_b200 as vx
+
+    rng = np.random.default_rng(31)
+    for it in range(160):
+        d = 1 + it % 4
+        per = bool(it % 2)
+        L = rng.uniform(0.5, 2.0, d)
+        counts = [int(c) for c in rng.integers(1, {1: 300, 2: 60, 3: 24, 4: 12}[d], d)]
+        grid = vx.VoxelGrid(counts, vx.Domain(list(L), vx.Boundary.Periodic if per else vx.Boundary.NonPeriodic))
+        c = rng.uniform(-0.2, 1.2, d) * L
+        if it % 5 == 0:  # radius exactly the distance to a voxel centre
+            k = [int(rng.integers(n)) for n in counts]
+            x = [(k[a] + 0.5) * grid.spacing[a] for a in range(d)]
+            r = float(np.sqrt(sum((c[a] - x[a]) ** 2 for a in range(d))))
+        else:
+            r = float(rng.uniform(0.0, 1.2) * np.sqrt((L ** 2).sum()))
+        ref = oracle.ref_ball_voxels(counts, L, per, c, r)
+        got = vx.ball_voxels(c, r, grid)
+        assert np.array_equal(got, ref), (it, got.size, ref.size)
+    with pytest.raises(ValueError, match="ball radius must be nonnegative"):
+        vx.ball_voxels([0.5], -1.0, vx.VoxelGrid([4], vx.Domain([1.0])))
+    with pytest.raises(ValueError, match="ball center dimension does not match the grid"):
+        vx.ball_voxels([0.5, 0.5], 0.1, vx.VoxelGrid([4], vx.Domain([1.0])))
