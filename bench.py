@@ -318,7 +318,15 @@ def run_ours(args):
         import torch.distributed as dist
 
         if args.dist_backend == "nccl":
+            # NCCL's communicator lines (rank count, NVLS / P2P transport) on
+            # stderr, so the run's log shows the N it ran on; stdout keeps the
+            # one JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+            log(f"rank {rank}/{world}: NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}, "
+                f"device cuda:{dev} {torch.cuda.get_device_name(dev)}")
         else:
             dist.init_process_group("gloo")
     c, box, grid, sites = make_inputs(args.config)
@@ -388,6 +396,33 @@ def run_ours(args):
     value = nv_total / (ms_per_step * 1e-3) / 1e9
     hist_sum = int(hist_d.sum().item())
     launches = int(sum(s["kernel_launches"] for s in stats))
+
+    # ---- optional image gather to rank 0 over NCCL (device tensors), timed
+    # apart from the labelling (north_star: "optionally gather the image") ----
+    gather = None
+    if dist is not None and args.dist_backend == "nccl":
+        from paper_2201_13234_b200.distributed import reduce_and_gather
+
+        sizes = [(vx.slab_bounds(n, r, world)[1] - vx.slab_bounds(n, r, world)[0]) * plane for r in range(world)]
+        g_ms = []
+        for k in range(3):
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            img = reduce_and_gather(labels_d, torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}"), sizes,
+                                    gather=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            g_ms.append(e0.elapsed_time(e1))
+        gt = torch.tensor([float(np.median(g_ms))], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+        gather = {"ms": float(gt.item()), "bytes_to_rank0": int(4 * nv_total),
+                  "note": "dist.gather of every slab to rank 0 (device tensors, NCCL), max over ranks; "
+                          "not part of value"}
+        if rank == 0 and img is not None:
+            gather["image_equal_slab0"] = bool(torch.equal(img[: nvs], labels_d))
+        del img
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
@@ -476,6 +511,7 @@ def run_ours(args):
                    "CUDA-graph replay of the captured per-step pipeline") +
                   (f" + {args.dist_backend.upper()} histogram all-reduce" if world > 1 else ""),
         "clocks": clk.summary(),
+        "gather": gather,
         "e2e": e2e,
         "gpu_launches": launches,
         "roofline": roofline,

@@ -8,6 +8,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <cstdlib>
+
 #include "vx_internal.cuh"
 
 namespace vxb {
@@ -55,6 +57,11 @@ __global__ void keys_kernel(Geo g, const double* __restrict__ p3, const double* 
   double tv = 0.0;
   if (s < g.n_sites) {
     alive = !(dropped && dropped[s]);
+    if (alive && g.win_on) {  // slab window (multi-GPU ranks): bin the slab's neighbourhood only
+      double u = p3[3 * s + 2] - g.win_c;
+      if (g.periodic) u -= floor(u * g.invL[2] + 0.5) * g.L[2];
+      alive = fabs(u) <= g.win_half;
+    }
     unsigned key = (unsigned)g.n_cells;
     if (alive) {
       const int cx = cell_of(p3[3 * s + 0], g.inv_cw[0], g.m[0]);
@@ -81,6 +88,20 @@ __global__ void keys_kernel(Geo g, const double* __restrict__ p3, const double* 
   }
 }
 
+// Counting sort (Voronoi): each alive site takes the next free slot of its cell
+// (cell_start = exclusive scan of the counts).  The order inside a cell is
+// then arbitrary -- every consumer orders candidates by site index (the ball
+// kernels' rank sort) or compares (prox, index) lexicographically (shell,
+// sub-brick shell), and pruning is an OR -- so labels do not depend on it.
+__global__ void place_kernel(long long n, const unsigned* __restrict__ keys, const int* __restrict__ cell_start,
+                             int* __restrict__ fill, int* __restrict__ vals_out, long long n_cells) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const unsigned k = keys[s];
+  if (k >= (unsigned)n_cells) return;  // dropped / outside the slab window
+  vals_out[cell_start[k] + atomicAdd(&fill[k], 1)] = (int)s;
+}
+
 __global__ void gather_kernel(long long n, const int* __restrict__ vals,
                               const double* __restrict__ p3, const double* __restrict__ t,
                               double* __restrict__ bx, double* __restrict__ by,
@@ -88,8 +109,9 @@ __global__ void gather_kernel(long long n, const int* __restrict__ vals,
                               int* __restrict__ bidx, float4* __restrict__ f4,
                               const int* __restrict__ cell_start, long long n_cells, DevCounters* ctr) {
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (p == 0) ctr->n_alive = (unsigned long long)cell_start[n_cells];  // dropped sites sort last
-  if (p >= n) return;
+  const long long n_alive = cell_start[n_cells];
+  if (p == 0) ctr->n_alive = (unsigned long long)n_alive;  // dropped sites sort last (radix) / are not placed
+  if (p >= n || p >= n_alive) return;
   const int s = vals[p];
   const double x = p3[3 * (long long)s + 0], y = p3[3 * (long long)s + 1],
                z = p3[3 * (long long)s + 2];
@@ -128,7 +150,7 @@ int launch_ingest(const Geo& g, const Len16& len, int dim_in, const double* pos_
 int launch_bin(const Geo& g, const double* p3, const double* t, const uint8_t* dropped,
                void* cub_tmp, size_t cub_tmp_bytes, unsigned* keys_a, unsigned* keys_b,
                int* vals_a, int* vals_b, double* bx, double* by, double* bz, double* bt,
-               int* bidx, float4* f4, int* cell_start, DevParams* prm, DevCounters* ctr,
+               int* bidx, float4* f4, int* cell_start, int* fill, DevParams* prm, DevCounters* ctr,
                cudaStream_t st) {
   const int T = 256;
   const unsigned nb = (unsigned)((g.n_sites + T - 1) / T);
@@ -137,16 +159,31 @@ int launch_bin(const Geo& g, const double* p3, const double* t, const uint8_t* d
   if (e != cudaSuccess) return -1000 - (int)e;
   keys_kernel<<<nb, T, 0, st>>>(g, p3, t, dropped, keys_a, vals_a, cell_start, prm);
   size_t bytes = cub_tmp_bytes;
-  // stable: equal cells keep ascending site order, as before
-  e = cub::DeviceRadixSort::SortPairs(cub_tmp, bytes, keys_a, keys_b, vals_a, vals_b,
-                                                  (int)g.n_sites, 0, key_bits(g.n_cells), st);
-  if (e != cudaSuccess) return -1000 - (int)e;
+  // Voronoi: counting sort (no radix passes).  Timed kinds keep the stable
+  // radix sort: the t0 cost scan samples the binned order, so a deterministic
+  // order keeps the reported parameter reproducible.
+  static const bool radix_env = std::getenv("VX_RADIX_BIN") != nullptr;
+  const bool counting = g.kind == kVoronoi && fill != nullptr && !radix_env;
+  int passes = 0;
+  if (!counting) {
+    // stable: equal cells keep ascending site order
+    e = cub::DeviceRadixSort::SortPairs(cub_tmp, bytes, keys_a, keys_b, vals_a, vals_b,
+                                        (int)g.n_sites, 0, key_bits(g.n_cells), st);
+    if (e != cudaSuccess) return -1000 - (int)e;
+    passes = 2 * ((key_bits(g.n_cells) + 7) / 8);
+  }
   bytes = cub_tmp_bytes;
   e = cub::DeviceScan::ExclusiveSum(cub_tmp, bytes, cell_start, cell_start, (int)(g.n_cells + 1), st);
   if (e != cudaSuccess) return -1000 - (int)e;
+  if (counting) {
+    e = cudaMemsetAsync(fill, 0, sizeof(int) * (size_t)g.n_cells, st);
+    if (e != cudaSuccess) return -1000 - (int)e;
+    place_kernel<<<nb, T, 0, st>>>(g.n_sites, keys_a, cell_start, fill, vals_b, g.n_cells);
+    passes = 1;
+  }
   gather_kernel<<<nb, T, 0, st>>>(g.n_sites, vals_b, p3, t, bx, by, bz, bt, bidx, f4, cell_start, g.n_cells,
                                   ctr);
-  return 4 + 2 * ((key_bits(g.n_cells) + 7) / 8);  // ours + CUB's onesweep and scan passes (approx.)
+  return 4 + passes;  // ours + the sort / placement and scan passes (approx.)
 }
 
 }  // namespace vxb

@@ -79,7 +79,7 @@ struct vx_context {
   std::mutex mu;
   Buf pos_raw, t_raw, w_raw, p3, t, dropped, keys_a, keys_b, vals_a, vals_b, bx, by, bz, bt, bidx,
       cell_start, cub, labels, dist, hist, unres, params, counters, scratch, vsample, vlab, vdist,
-      vbad, slots, f4, sb_info, sb_list, sb_count, sb_slots, sb_ovf, ctab, nd_x, nd_t, nd_idx, nd_cells;
+      vbad, slots, f4, sb_info, sb_list, sb_count, sb_slots, sb_ovf, ctab, nd_x, nd_t, nd_idx, nd_cells, cell_fill;
   DevParams* h_prm = nullptr;
   DevCounters* h_ctr = nullptr;
   cudaEvent_t ev[8] = {};  // stage markers (options.profile_stages)
@@ -100,11 +100,11 @@ struct vx_context {
   // default contexts when their thread exits, and a failed create_context.
   ~vx_context();
 
-  Buf* all[40] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
+  Buf* all[41] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
                   &vals_a,  &vals_b,  &bx,    &by,    &bz,     &bt,      &bidx,     &cell_start,
                   &cub,     &labels,  &dist,  &hist,  &unres,  &params,  &counters, &scratch,
                   &vsample, &vlab,    &vdist, &vbad,  &slots,  &f4,      &sb_info,  &sb_list,
-                  &sb_count, &sb_slots, &sb_ovf, &ctab, &nd_x,  &nd_t,   &nd_idx,   &nd_cells};
+                  &sb_count, &sb_slots, &sb_ovf, &ctab, &nd_x,  &nd_t,   &nd_idx,   &nd_cells, &cell_fill};
 };
 
 namespace {
@@ -861,15 +861,38 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       bins.cell_start = cs;
       float4* f4 = ensure<float4>(ctx->f4, (size_t)ns);
       bins.f4 = f4;
+      bins.win_r2 = 0.0;
+      bins.all_p3 = p3;
+      bins.n_all = ns;
+      // Slab window (a rank's z-slab of a multi-GPU run, Voronoi): bin only the
+      // sites within M = 2 R + 2 cells + 2 voxels of the slab along z.  The ball
+      // phase gathers within R < M; a shell search whose best distance reaches
+      // M is redone over all sites (shell.cu / subshell.cu), so labels stay exact.
+      if (!timed(P) && d == 3 && (ze - zb) < n_last && !std::getenv("VX_NO_WINDOW")) {
+        const double R = (O.has_override ? O.override_param
+                                         : (ns == 1 ? cover_radius(d, P->lengths, P->periodic)
+                                                    : optimal_r0(ns, d, P->lengths) * ball_scale)) *
+                             (1.0 + 1e-9) + 1e-12 * g.lmax;
+        const double M = 2.0 * R + 2.0 * g.cw[2] + 2.0 * g.sp[2];
+        const double zlo = ((double)zb + 0.5) * g.sp[2], zhi = ((double)(ze - 1) + 0.5) * g.sp[2];
+        const double half = 0.5 * (zhi - zlo) + M;
+        if (2.0 * half < 0.9 * g.L[2]) {
+          g.win_on = 1;
+          g.win_c = 0.5 * (zlo + zhi);
+          g.win_half = half;
+          const double m1 = M * (1.0 - 1e-9);
+          bins.win_r2 = m1 * m1 * (1.0 - 1e-9);
+        }
+      }
       if (do_prune) {
         launches += bin_checked(g, p3, tdev, nullptr, cub, cub_bytes, ka, kb, va, vb, bx, by, bz, bt,
-                                bidx, f4, cs, prm, ctr, st);
+                                bidx, f4, cs, ensure<int>(ctx->cell_fill, (size_t)g.n_cells + 1), prm, ctr, st);
         dbg(st, "bin0");
         launches += launch_prune(g, bins, p3, tdev, prm, dropped, st);
         dbg(st, "prune");
       }
       launches += bin_checked(g, p3, tdev, dropped, cub, cub_bytes, ka, kb, va, vb, bx, by, bz, bt,
-                              bidx, f4, cs, prm, ctr, st);
+                              bidx, f4, cs, ensure<int>(ctx->cell_fill, (size_t)g.n_cells + 1), prm, ctr, st);
       dbg(st, "bin");
       tm.mark(2);
       if (!timed(P))
@@ -1266,7 +1289,7 @@ int vx_prune(vx_context* ctx_in, const vx_problem* P, uint8_t* dropped_out, int6
       bins.stride = ns;
       bins.f4 = nullptr;
       bin_checked(g, p3, tdev, nullptr, cub, cub_bytes, ka, kb, va, vb, bx, by, bz, bt, bidx,
-                  (float4*)nullptr, cs, prm, ctr, st);
+                  (float4*)nullptr, cs, nullptr, prm, ctr, st);
       launch_prune(g, bins, p3, tdev, prm, dropped, st);
     } else {
       launch_prune_generic(P->kind, P->periodic, d, P->lengths, P->growth, pos, tdev, ns, dropped, st);

@@ -64,6 +64,32 @@ __device__ void shell_all(const Geo& g, const Bins& bins, int n_alive, long long
       bi = oi;
     }
   }
+  if (KIND == kVoronoi && bins.win_r2 > 0.0 && !(best < bins.win_r2)) {
+    // an unbinned site (beyond the slab window) may be nearer: all sites
+    double b2 = __longlong_as_double(0x7ff0000000000000ll);
+    int i2 = 0x7fffffff;
+    for (long long s = lane; s < bins.n_all; s += 32) {
+      const double* q = bins.all_p3 + 3 * s;
+      const double dsq = __dadd_rn(__dadd_rn(axis_sq<PER>(q[2], c[2], g.L[2], g.invL[2]),
+                                             axis_sq<PER>(q[1], c[1], g.L[1], g.invL[1])),
+                                   axis_sq<PER>(q[0], c[0], g.L[0], g.invL[0]));
+      if (dsq < b2 || (dsq == b2 && (int)s < i2)) {
+        b2 = dsq;
+        i2 = (int)s;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, b2, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, i2, o);
+      if (ob < b2 || (ob == b2 && oi < i2)) {
+        b2 = ob;
+        i2 = oi;
+      }
+    }
+    best = b2;
+    bi = i2;
+  }
   if (lane == 0) {
     const long long out = lin - g.z_begin * g.n[0] * g.n[1];
     labels[out] = bi;
@@ -191,6 +217,33 @@ __device__ void shell_one(const Geo& g, const Bins& bins, const DevParams* prm, 
       phi[a] = hi[a];
       pfull[a] = full[a];
     }
+  }
+  if (KIND == kVoronoi && bins.win_r2 > 0.0 && !(best < bins.win_r2)) {
+    // an unbinned site (beyond the slab window) may be nearer: all sites, lanes striding
+    double b2 = __longlong_as_double(0x7ff0000000000000ll);
+    int i2 = 0x7fffffff;
+    for (long long s = lane; s < bins.n_all; s += 32) {
+      const double* q = bins.all_p3 + 3 * s;
+      const double dsq = __dadd_rn(__dadd_rn(axis_sq<PER>(q[2], c[2], g.L[2], g.invL[2]),
+                                             axis_sq<PER>(q[1], c[1], g.L[1], g.invL[1])),
+                                   axis_sq<PER>(q[0], c[0], g.L[0], g.invL[0]));
+      if (dsq < b2 || (dsq == b2 && (int)s < i2)) {
+        b2 = dsq;
+        i2 = (int)s;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, b2, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, i2, o);
+      if (ob < b2 || (ob == b2 && oi < i2)) {
+        b2 = ob;
+        i2 = oi;
+      }
+    }
+    best = b2;
+    bi = i2;
+    ne += (unsigned long long)bins.n_all;
   }
   if (lane == 0) {
     const long long out = lin - g.z_begin * g.n[0] * g.n[1];

@@ -184,6 +184,18 @@ __global__ void __launch_bounds__(kThreads)
         pfull[a] = full[a];
       }
     }
+    if (KIND == kVoronoi && bins.win_r2 > 0.0) {  // slab window: unbinned sites may be nearer
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        if (!(best[v] < bins.win_r2)) {
+          const double cv[3] = {cxs[v & 3], cys[v >> 2], czs};
+          double b2;
+          int i2;
+          allsites_min<PER>(g, bins, cv, b2, i2);
+          best[v] = b2;
+          bi[v] = i2;
+        }
+    }
     // stores (voxels of the grid only) and histogram runs
     const long long lin0 = x0 + qx + g.n[0] * (y0 + vy + g.n[1] * (z0 + vz)) - slab_base;
     int run_id = -1;

@@ -92,3 +92,85 @@ def test_slab_decomposition_gloo(world, nz):
         assert np.array_equal(h, hist)
         assert h.sum() == p.n_voxels
     assert np.array_equal(got[0][4], full)
+
+
+def _two_gpus():
+    import torch
+
+    return torch.cuda.is_available() and torch.cuda.device_count() >= 2
+
+
+@pytest.mark.gpu
+def test_torchrun_two_ranks_nccl_bench():
+    """bench.py under torchrun with two ranks over NCCL (needs >= 2 GPUs; the
+    one-GPU test box skips it): one JSON line from rank 0 with n_gpus 2, the
+    histogram reduced over both slabs, the device-side gather timed apart."""
+    if not _two_gpus():
+        pytest.skip("needs >= 2 GPUs")
+    import json
+    import subprocess
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--config", "1"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["gather"]["ms"] > 0
+    assert d["parity"]["histogram_sum_ok"] is True
+    assert "nRanks 2" in out.stderr or "nranks 2" in out.stderr.lower()
+
+
+def _nccl_worker(rank, world, port, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        sys.path.insert(0, ROOT)
+        import torch
+        import torch.distributed as dist
+
+        import oracle
+        from paper_2201_13234_b200.distributed import tessellate_slabs_device
+        from paper_2201_13234_b200.engine import Tessellator
+
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+        p = _problem(23)
+        pos = torch.from_numpy(p.positions).cuda()
+        t = torch.from_numpy(p.times).cuda()
+        eng = Tessellator(rank)
+        lab, hist, img, (z0, z1) = tessellate_slabs_device(
+            eng, kind=p.kind, counts=list(p.counts), lengths=list(p.lengths), periodic=p.periodic, positions=pos,
+            times=t, growth=p.growth, gather=True)
+        q.put((rank, hist.cpu().numpy(), None if img is None else img.cpu().numpy()))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, "error", repr(e)))
+
+
+@pytest.mark.gpu
+def test_device_slabs_two_ranks_nccl():
+    """tessellate_slabs_device on two GPUs over NCCL: the gathered image and the
+    reduced histogram equal the single-process oracle result (>= 2 GPUs)."""
+    if not _two_gpus():
+        pytest.skip("needs >= 2 GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    got = sorted([q.get(timeout=300) for _ in range(2)], key=lambda g: g[0])
+    for pr in procs:
+        pr.join(timeout=60)
+    for g in got:
+        assert not (isinstance(g[1], str) and g[1] == "error"), g[2]
+    import oracle
+
+    p = _problem(23)
+    full, _ = oracle.brute(p, distances=False)
+    hist = np.bincount(full, minlength=p.n_sites)
+    assert np.array_equal(got[0][2].view(np.uint32), full)
+    for g in got:
+        assert np.array_equal(g[1], hist)

@@ -1065,3 +1065,30 @@ def test_extreme_domain_scales_vs_oracle(oracle_mod, scale, kind):
         r = run_fast(p, prune=False, distances=True)
         assert np.array_equal(r.labels.labels, lab), int((r.labels.labels != lab).sum())
         assert np.array_equal(bits(r.distances.values), bits(dist))
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+def test_slab_window_binning_fallback_vs_oracle(oracle_mod, periodic):
+    """A rank's slab bins only the sites within a window of 2 R + 2 cells along
+    z (Voronoi).  With a small override radius most voxels are unresolved and
+    many have their nearest site outside the window: the shell searches must
+    fall back to all sites and stay exact (labels, distances, histogram)."""
+    import paper_2201_13234_b200 as vx
+
+    rng = np.random.default_rng(61 + periodic)
+    counts = [40, 36, 120]
+    L = np.array([1.0, 0.9, 3.0])
+    ns = 400
+    pos, _ = oracle_mod.generate_uniform_sites(3, L, ns, 0, 1.0, int(rng.integers(1 << 40)))
+    p = oracle_mod.Problem(0, counts, L, periodic, pos)
+    lab, dist = oracle_mod.brute(p)
+    plane = counts[0] * counts[1]
+    sites, grid = to_vx(p)
+    for (a, b), r0 in (((50, 62), 0.02), ((0, 9), 0.005), ((111, 120), 0.05)):
+        r = vx.tessellate_fast(sites, grid, vx.FastOptions(override_param=r0), distances=True, histogram=True,
+                               slab=(a, b))
+        ref = lab[a * plane: b * plane]
+        assert np.array_equal(r.labels.labels, ref), (a, b, int((r.labels.labels != ref).sum()))
+        assert np.array_equal(bits(r.distances.values), bits(dist[a * plane: b * plane]))
+        assert np.array_equal(r.histogram, np.bincount(ref, minlength=ns).astype(np.uint64))
+        assert r.stats["n_unresolved"] > 0
