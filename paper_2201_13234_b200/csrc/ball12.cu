@@ -75,6 +75,7 @@ struct __align__(16) WarpSmem {
   int L[kLcapD];       // dense mode: a sub-brick's survivors (binned positions)
   float4 bxy;          // the column's x/y box (c[0], c[1], h[0], h[1]), shared by its sub-bricks
   unsigned evals;      // exact evaluations the eval kernel will do for this warp's sub-bricks
+  alignas(16) float zref[16];  // the sub-brick's reference site: SiteF fields + flags (written by its lane)
 };
 
 // eval12: per warp (one sub-brick); LC = list capacity
@@ -167,11 +168,13 @@ __device__ __forceinline__ bool bisector_keep(const SiteF& s, unsigned fs, const
                                               unsigned f0, const FBox& B, const float* halfL,
                                               float invG, float e_d) {
   float D = 0.f, mag = 0.f;
+  // neither site near half a period (flag bits 3..5): no axis needs the wrap bound
+  const bool anyrisk = PER && ((fs | f0) & 0x38u) != 0u;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const bool wrapcase = PER && (((fs | f0) >> a) & 1u ||
-                                  fabsf(s.v[a]) + B.h[a] > halfL[a] * (1.f - 1e-5f) ||
-                                  fabsf(z.v[a]) + B.h[a] > halfL[a] * (1.f - 1e-5f));
+    const bool wrapcase = anyrisk && (((fs | f0) >> a) & 1u ||
+                                      fabsf(s.v[a]) + B.h[a] > halfL[a] * (1.f - 1e-5f) ||
+                                      fabsf(z.v[a]) + B.h[a] > halfL[a] * (1.f - 1e-5f));
     float term, m;
     if (wrapcase) {
       term = s.mn[a] * s.mn[a] - z.mx[a] * z.mx[a];
@@ -390,6 +393,9 @@ __global__ void __launch_bounds__(kB2Threads, 4)
           if (PER) {
             u = u - floor(u * g.invL[a] + 0.5) * g.L[a];
             if (fabs(u) + hs[a] >= g.halfL[a] * (1.0 - 1e-7) - 4.0 * e_d) fl |= 1u << a;
+            // bit 3 + a: some box inside the super-brick may see the site near
+            // half a period (a superset of bisector_keep's per-axis test)
+            if (fabs(u) + hs[a] + 8.0 * e_d >= g.halfL[a] * (1.0 - 2e-5)) fl |= 8u << a;
           }
           uf[a] = (float)u;
           const double m = ((fl >> a) & 1u) ? 0.0 : fmax(fabs(u) - hs[a], 0.0);
@@ -677,19 +683,31 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       for (int o = 16; o > 0; o >>= 1) km = min(km, __shfl_xor_sync(0xffffffffu, km, o));
       const int r0 = (int)(km & 63u), rl = r0 & 31;
       const bool rhi = r0 >= 32;
-      // broadcast the reference's bounds from its owner lane
-      SiteF z;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        z.v[a] = __shfl_sync(0xffffffffu, rhi ? sb.v[a] : sa.v[a], rl);
-        z.mn[a] = __shfl_sync(0xffffffffu, rhi ? sb.mn[a] : sa.mn[a], rl);
-        z.mx[a] = __shfl_sync(0xffffffffu, rhi ? sb.mx[a] : sa.mx[a], rl);
+      // the reference's bounds through shared memory, written by its owner lane
+      if (lane == rl) {
+        const SiteF& o = rhi ? sb : sa;
+        float* zr = ws.zref;
+        zr[0] = o.v[0], zr[1] = o.v[1], zr[2] = o.v[2];
+        zr[3] = o.mn[0], zr[4] = o.mn[1], zr[5] = o.mn[2];
+        zr[6] = o.mx[0], zr[7] = o.mx[1], zr[8] = o.mx[2];
+        zr[9] = o.t, zr[10] = o.lb, zr[11] = o.ub, zr[12] = o.ubp;
+        zr[13] = __uint_as_float(rhi ? flb : fla);
       }
-      z.t = __shfl_sync(0xffffffffu, rhi ? sb.t : sa.t, rl);
-      z.lb = __shfl_sync(0xffffffffu, rhi ? sb.lb : sa.lb, rl);
-      z.ub = __shfl_sync(0xffffffffu, rhi ? sb.ub : sa.ub, rl);
-      const float tau = fminf(__shfl_sync(0xffffffffu, rhi ? sb.ubp : sa.ubp, rl), tcf);
-      const unsigned fl0 = __shfl_sync(0xffffffffu, rhi ? flb : fla, rl);
+      __syncwarp();
+      SiteF z;
+      {
+        const float4 q0 = *reinterpret_cast<const float4*>(&ws.zref[0]);
+        const float4 q1 = *reinterpret_cast<const float4*>(&ws.zref[4]);
+        const float4 q2 = *reinterpret_cast<const float4*>(&ws.zref[8]);
+        const float2 q3 = *reinterpret_cast<const float2*>(&ws.zref[12]);
+        z.v[0] = q0.x, z.v[1] = q0.y, z.v[2] = q0.z;
+        z.mn[0] = q0.w, z.mn[1] = q1.x, z.mn[2] = q1.y;
+        z.mx[0] = q1.z, z.mx[1] = q1.w, z.mx[2] = q2.x;
+        z.t = q2.y, z.lb = q2.z, z.ub = q2.w;
+        z.ubp = q3.x;
+      }
+      const float tau = fminf(z.ubp, tcf);
+      const unsigned fl0 = __float_as_uint(ws.zref[13]);
       const bool ka = va && (lane == r0 || (sa.lbp <= tau &&
                                             bisector_keep<KIND, PER>(sa, fla, z, fl0, Bs, halfLf, invG, e_d)));
       const bool kb = vb && (lane + 32 == r0 || (sb.lbp <= tau &&

@@ -159,11 +159,9 @@ int launch_bin(const Geo& g, const double* p3, const double* t, const uint8_t* d
   if (e != cudaSuccess) return -1000 - (int)e;
   keys_kernel<<<nb, T, 0, st>>>(g, p3, t, dropped, keys_a, vals_a, cell_start, prm);
   size_t bytes = cub_tmp_bytes;
-  // Voronoi: counting sort (no radix passes).  Timed kinds keep the stable
-  // radix sort: the t0 cost scan samples the binned order, so a deterministic
-  // order keeps the reported parameter reproducible.
+  // counting sort (no radix passes); VX_RADIX_BIN=1: the stable radix sort
   static const bool radix_env = std::getenv("VX_RADIX_BIN") != nullptr;
-  const bool counting = g.kind == kVoronoi && fill != nullptr && !radix_env;
+  const bool counting = fill != nullptr && !radix_env;
   int passes = 0;
   if (!counting) {
     // stable: equal cells keep ascending site order

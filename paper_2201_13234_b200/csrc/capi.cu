@@ -800,13 +800,11 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       dbg(st, "bin");
       tm.mark(2);
       if (!timed(P)) r0 = ns == 1 ? cover_radius(d, P->lengths, P->periodic) : optimal_r0(ns, d, P->lengths);
-      Bins bt;
-      std::memset(&bt, 0, sizeof(bt));
-      bt.t = nt;
       Geo gp = g;  // the cost model reads kind, dim, growth, volume, lengths
       gp.lmax = gn.lmax;
       double* scratch = ensure<double>(ctx->scratch, 1024);
-      launches += launch_params(gp, bt, prm, ctr, O.has_override, O.override_param, r0, ball_scale, scratch, st);
+      launches += launch_params(gp, tdev, dropped, prm, ctr, O.has_override, O.override_param, r0, ball_scale,
+                                scratch, st);
       dbg(st, "params");
       tm.mark(3);
       const long long cap = (long long)std::min<int64_t>(nvs, 1ll << 26);
@@ -897,7 +895,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       tm.mark(2);
       if (!timed(P))
         r0 = ns == 1 ? cover_radius(d, P->lengths, P->periodic) : optimal_r0(ns, d, P->lengths);
-      launches += launch_params(g, bins, prm, ctr, O.has_override, O.override_param, r0,
+      launches += launch_params(g, tdev, dropped, prm, ctr, O.has_override, O.override_param, r0,
                                 ball_scale, scratch, st);
       trace.rec(5, st);
       dbg(st, "params");

@@ -13,7 +13,7 @@
 namespace vxb {
 
 constexpr int kScan = 256;
-constexpr long long kCostSample = 8192;
+constexpr long long kCostSample = 4096;
 
 __global__ void init_kernel(DevParams* prm, DevCounters* ctr) {
   prm->tmin_key = ~0ull;
@@ -63,38 +63,71 @@ __device__ void scan_range(const CostArgs& a, const DevParams* prm, const double
     *hi = bhi;
     return;
   }
-  int best = 0;
-  for (int i = 1; i < kScan; ++i)
-    if (costs0[i] < costs0[best]) best = i;
+  const int best = (int)costs0[2 * kScan];  // pass 0's arg-min (argmin_kernel)
   const double step = (bhi - blo) / (kScan - 1);
   const double bt = blo + (bhi - blo) * best / (kScan - 1);
   *lo = fmax(blo, bt - step);
   *hi = fmin(bhi, bt + step);
 }
 
+// first arg-min of costs[0, kScan) (lowest index on ties, as a serial scan),
+// by one warp
+__device__ void argmin_warp(const double* c, int* out) {
+  const int lane = threadIdx.x & 31;
+  double bv = __longlong_as_double(0x7ff0000000000000ll);
+  int bi = 0x7fffffff;
+  for (int i = lane; i < kScan; i += 32)
+    if (c[i] < bv) {
+      bv = c[i];
+      bi = i;
+    }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov < bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  *out = bi == 0x7fffffff ? 0 : bi;
+}
+__device__ void argmin_pair(const double* costs, int* b0, int* b1) {
+  argmin_warp(costs, b0);
+  argmin_warp(costs + kScan, b1);
+}
+__global__ void argmin_kernel(double* costs) {  // after pass 0: its arg-min for pass 1's bracket
+  int b;
+  argmin_warp(costs, &b);
+  if (threadIdx.x == 0) costs[2 * kScan] = (double)b;
+}
+
 // growth_cost(t0)/N_v = sum v'_s/V + N_s * prod(1 - v'_s/V), one CTA per t0.
-__global__ void cost_scan_kernel(CostArgs a, const double* __restrict__ bt,
-                                 const DevCounters* ctr, const DevParams* prm, double* costs,
+__global__ void cost_scan_kernel(CostArgs a, const double* __restrict__ t_orig, const uint8_t* __restrict__ dropped,
+                                 long long n_sites, const DevCounters* ctr, const DevParams* prm, double* costs,
                                  int pass) {
   __shared__ double s_sum[32], s_log[32];
+  __shared__ int s_cnt[32];
   double lo, hi;
   scan_range(a, prm, costs, pass, &lo, &hi);
   const double t0 = lo + (hi - lo) * blockIdx.x / (kScan - 1);
   const long long n = (long long)ctr->n_alive;
   // t0 only sizes the ball phase (labels never depend on it): an evenly
-  // strided sample of <= kCostSample sites estimates the sums (binned order is
-  // spatial, independent of the birth times), scaled back to n
-  const long long m = n < kCostSample ? n : kCostSample;
+  // strided sample of <= kCostSample sites in ORIGINAL order (independent of
+  // the binned order, so the choice is reproducible), pruned ones skipped,
+  // scaled back to the n alive sites
+  const long long m = n_sites < kCostSample ? n_sites : kCostSample;
   double sum = 0.0, lg = 0.0;
+  int cnt = 0;
   for (long long i = threadIdx.x; i < m; i += blockDim.x) {
-    const double f = site_frac(a, t0, bt[i * n / m]);
+    const long long s = i * n_sites / m;
+    if (dropped && dropped[s]) continue;
+    const double f = site_frac(a, t0, t_orig[s]);
     sum += f;
     lg += log1p(-f);
+    ++cnt;
   }
-  if (m < n) {
-    sum *= (double)n / (double)m;
-    lg *= (double)n / (double)m;
-  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0) s_cnt[threadIdx.x >> 5] = cnt;
   for (int o = 16; o > 0; o >>= 1) {
     sum += __shfl_xor_sync(0xffffffffu, sum, o);
     lg += __shfl_xor_sync(0xffffffffu, lg, o);
@@ -106,9 +139,15 @@ __global__ void cost_scan_kernel(CostArgs a, const double* __restrict__ bt,
   __syncthreads();
   if (threadIdx.x == 0) {
     double S = 0.0, Lg = 0.0;
+    long long C = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
       S += s_sum[w];
       Lg += s_log[w];
+      C += s_cnt[w];
+    }
+    if (C > 0 && C < n) {
+      S *= (double)n / (double)C;
+      Lg *= (double)n / (double)C;
     }
     costs[pass * kScan + blockIdx.x] = S + (double)n * exp(Lg);
   }
@@ -116,7 +155,10 @@ __global__ void cost_scan_kernel(CostArgs a, const double* __restrict__ bt,
 
 __global__ void timed_finalize_kernel(CostArgs a, DevParams* prm, const DevCounters* ctr,
                                       const double* costs, int has_override, double override_t0,
-                                      double lmax) {
+                                      double lmax) {  // one warp
+  int b0 = 0, b1 = 0;
+  if (!has_override && ctr->n_alive > 1) argmin_pair(costs, &b0, &b1);
+  if (threadIdx.x != 0) return;
   const double t_min = dkey_inv(prm->tmin_key);
   prm->t_min = t_min;
   prm->t_max = dkey_inv(prm->tmax_key);
@@ -129,11 +171,7 @@ __global__ void timed_finalize_kernel(CostArgs a, DevParams* prm, const DevCount
     double lo0, hi0, lo1, hi1;
     scan_range(a, prm, costs, 0, &lo0, &hi0);
     scan_range(a, prm, costs, 1, &lo1, &hi1);
-    int b0 = 0, b1 = 0;
-    for (int i = 1; i < kScan; ++i) {
-      if (costs[i] < costs[b0]) b0 = i;
-      if (costs[kScan + i] < costs[kScan + b1]) b1 = i;
-    }
+
     t0 = costs[kScan + b1] <= costs[b0] ? lo1 + (hi1 - lo1) * b1 / (kScan - 1)
                                         : lo0 + (hi0 - lo0) * b0 / (kScan - 1);
   }
@@ -148,8 +186,8 @@ __global__ void timed_finalize_kernel(CostArgs a, DevParams* prm, const DevCount
                                                       : 3.0 * lmax * lmax / a.growth));
 }
 
-int launch_params(const Geo& g, const Bins& bins, DevParams* prm, const DevCounters* ctr,
-                  int has_override, double override_param, double r0, double ball_scale,
+int launch_params(const Geo& g, const double* t_orig, const uint8_t* dropped, DevParams* prm,
+                  const DevCounters* ctr, int has_override, double override_param, double r0, double ball_scale,
                   double* scratch, cudaStream_t st) {
   if (g.kind == kVoronoi) {
     const double R = has_override ? override_param : r0 * ball_scale;
@@ -171,12 +209,13 @@ int launch_params(const Geo& g, const Bins& bins, DevParams* prm, const DevCount
   }
   int n = 1;
   if (!has_override) {
-    cost_scan_kernel<<<kScan, 256, 0, st>>>(a, bins.t, ctr, prm, scratch, 0);
-    cost_scan_kernel<<<kScan, 256, 0, st>>>(a, bins.t, ctr, prm, scratch, 1);
-    n += 2;
+    cost_scan_kernel<<<kScan, 256, 0, st>>>(a, t_orig, dropped, g.n_sites, ctr, prm, scratch, 0);
+    argmin_kernel<<<1, 32, 0, st>>>(scratch);
+    cost_scan_kernel<<<kScan, 256, 0, st>>>(a, t_orig, dropped, g.n_sites, ctr, prm, scratch, 1);
+    n += 3;
   }
-  timed_finalize_kernel<<<1, 1, 0, st>>>(a, prm, ctr, scratch, has_override, override_param,
-                                         g.lmax);
+  timed_finalize_kernel<<<1, 32, 0, st>>>(a, prm, ctr, scratch, has_override, override_param,
+                                          g.lmax);
   return n;
 }
 

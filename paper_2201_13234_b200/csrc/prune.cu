@@ -28,11 +28,16 @@ __device__ __forceinline__ double axis_min_sq_diff(double a, double b, double L,
   return at0 < atL ? at0 : atL;
 }
 
+// One warp per site: the lanes split the cells of its reach box (one cell per
+// lane, its sites in turn); a ballot ORs the verdicts.
+constexpr int kPruneThreads = 128;
+
 template <bool PER>
-__global__ void prune_kernel(Geo g, Bins bins, const double* __restrict__ p3,
-                             const double* __restrict__ times, const DevParams* prm,
-                             uint8_t* __restrict__ dropped) {
-  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kPruneThreads)
+    prune_kernel(Geo g, Bins bins, const double* __restrict__ p3, const double* __restrict__ times,
+                 const DevParams* prm, uint8_t* __restrict__ dropped) {
+  const long long s = blockIdx.x * (long long)(kPruneThreads / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (s >= g.n_sites) return;
   const double xs[3] = {p3[3 * s], p3[3 * s + 1], p3[3 * s + 2]};
   const double ts = times[s];
@@ -61,41 +66,46 @@ __global__ void prune_kernel(Geo g, Bins bins, const double* __restrict__ p3,
       hi[a] = hi[a] >= g.m[a] ? g.m[a] - 1 : hi[a];
     }
   }
+  const long long nx = hi[0] - lo[0] + 1, ny = hi[1] - lo[1] + 1, nz = hi[2] - lo[2] + 1;
+  const long long ncell = nx > 0 && ny > 0 && nz > 0 ? nx * ny * nz : 0;
   bool drop = false;
-  for (long long cz = lo[2]; cz <= hi[2] && !drop; ++cz) {
-    const long long wz = PER ? ((cz % g.m[2]) + g.m[2]) % g.m[2] : cz;
-    for (long long cy = lo[1]; cy <= hi[1] && !drop; ++cy) {
+  for (long long c0 = 0; c0 < ncell; c0 += 32) {
+    const long long c = c0 + lane;
+    if (c < ncell) {
+      const long long cx = lo[0] + c % nx, cy = lo[1] + (c / nx) % ny, cz = lo[2] + c / (nx * ny);
+      const long long wx = PER ? ((cx % g.m[0]) + g.m[0]) % g.m[0] : cx;
       const long long wy = PER ? ((cy % g.m[1]) + g.m[1]) % g.m[1] : cy;
-      for (long long cx = lo[0]; cx <= hi[0] && !drop; ++cx) {
-        const long long wx = PER ? ((cx % g.m[0]) + g.m[0]) % g.m[0] : cx;
-        const long long cell = wx + (long long)g.m[0] * (wy + (long long)g.m[1] * wz);
-        const int b = bins.cell_start[cell], e = bins.cell_start[cell + 1];
-        for (int p = b; p < e; ++p) {
-          const long long o = bins.idx[p];
-          if (o == s) continue;
-          const double xo[3] = {bins.x[p], bins.y[p], bins.z[p]};
-          const double to = bins.t[p];
-          if (g.kind == kJohnsonMehl) {
-            // l_periodic_distance_sq(xs, xo): a = xs, b = xo (sites.cpp:136-139)
-            double acc = 0.0;
-            for (int i = 2; i >= 0; --i) acc = __dadd_rn(acc, axis_sq<PER>(xo[i], xs[i], g.L[i], g.invL[i]));
-            double reach = __dsqrt_rn(acc);
-            if (!g.g_is_one) reach = __ddiv_rn(reach, G);
-            reach = __dadd_rn(reach, to);
-            if (reach < ts || (reach == ts && o < s)) drop = true;
-          } else {
-            // ascending axis order; a padded axis adds exactly +0 (see Geo)
-            double margin = __dmul_rn(G, __dsub_rn(ts, to));
-            for (int i = 0; i < 3; ++i)
-              margin = __dadd_rn(margin, axis_min_sq_diff(xs[i], xo[i], g.L[i], g.invL[i], PER));
-            if (margin > 0.0 || (margin == 0.0 && o < s)) drop = true;
-          }
-          if (drop) break;
+      const long long wz = PER ? ((cz % g.m[2]) + g.m[2]) % g.m[2] : cz;
+      const long long cell = wx + (long long)g.m[0] * (wy + (long long)g.m[1] * wz);
+      const int b = bins.cell_start[cell], e = bins.cell_start[cell + 1];
+      for (int p = b; p < e && !drop; ++p) {
+        const long long o = bins.idx[p];
+        if (o == s) continue;
+        const double xo[3] = {bins.x[p], bins.y[p], bins.z[p]};
+        const double to = bins.t[p];
+        if (g.kind == kJohnsonMehl) {
+          // l_periodic_distance_sq(xs, xo): a = xs, b = xo (sites.cpp:136-139)
+          double acc = 0.0;
+          for (int i = 2; i >= 0; --i) acc = __dadd_rn(acc, axis_sq<PER>(xo[i], xs[i], g.L[i], g.invL[i]));
+          double reach = __dsqrt_rn(acc);
+          if (!g.g_is_one) reach = __ddiv_rn(reach, G);
+          reach = __dadd_rn(reach, to);
+          drop = reach < ts || (reach == ts && o < s);
+        } else {
+          // ascending axis order; a padded axis adds exactly +0 (see Geo)
+          double margin = __dmul_rn(G, __dsub_rn(ts, to));
+          for (int i = 0; i < 3; ++i)
+            margin = __dadd_rn(margin, axis_min_sq_diff(xs[i], xo[i], g.L[i], g.invL[i], PER));
+          drop = margin > 0.0 || (margin == 0.0 && o < s);
         }
       }
     }
+    if (__any_sync(0xffffffffu, drop)) {
+      drop = true;
+      break;
+    }
   }
-  dropped[s] = drop ? 1 : 0;
+  if (lane == 0) dropped[s] = drop ? 1 : 0;
 }
 
 // Any dimension (d >= 4 path): the reference's full O(N_s^2) double loop.
@@ -151,8 +161,8 @@ int launch_prune_generic(int kind, int periodic, int dim, const double* lengths,
 
 int launch_prune(const Geo& g, const Bins& bins, const double* p3, const double* times,
                  const DevParams* prm, uint8_t* dropped, cudaStream_t st) {
-  const int T = 128;
-  const unsigned nb = (unsigned)((g.n_sites + T - 1) / T);
+  const int T = kPruneThreads;
+  const unsigned nb = (unsigned)((g.n_sites + T / 32 - 1) / (T / 32));
   if (g.periodic) prune_kernel<true><<<nb, T, 0, st>>>(g, bins, p3, times, prm, dropped);
   else prune_kernel<false><<<nb, T, 0, st>>>(g, bins, p3, times, prm, dropped);
   return 1;
