@@ -51,11 +51,21 @@ __device__ __forceinline__ int cell_of(double v, double inv_cw, int m) {
 
 __global__ void keys_kernel(Geo g, const double* __restrict__ p3, const double* __restrict__ t,
                             const uint8_t* __restrict__ dropped, unsigned* __restrict__ keys,
-                            int* __restrict__ vals, int* __restrict__ counts, DevParams* prm) {
+                            int* __restrict__ vals, int* __restrict__ counts, DevParams* prm,
+                            unsigned* ctr_bad) {
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   bool alive = false;
   double tv = 0.0;
   if (s < g.n_sites) {
+    if (g.validate_in_keys) {  // sites.cpp:54-57: finite, strictly inside (0, L)
+      bool bad = false;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double v = p3[3 * s + a];
+        bad |= !(isfinite(v) && v > 0.0 && v < g.L[a]);
+      }
+      if (bad) atomicOr(&ctr_bad[0], 1u);
+    }
     alive = !(dropped && dropped[s]);
     if (alive && g.win_on) {  // slab window (multi-GPU ranks): bin the slab's neighbourhood only
       double u = p3[3 * s + 2] - g.win_c;
@@ -157,7 +167,7 @@ int launch_bin(const Geo& g, const double* p3, const double* t, const uint8_t* d
   // cell_start = exclusive scan of the per-cell site counts (counted in place)
   cudaError_t e = cudaMemsetAsync(cell_start, 0, sizeof(int) * (size_t)(g.n_cells + 1), st);
   if (e != cudaSuccess) return -1000 - (int)e;
-  keys_kernel<<<nb, T, 0, st>>>(g, p3, t, dropped, keys_a, vals_a, cell_start, prm);
+  keys_kernel<<<nb, T, 0, st>>>(g, p3, t, dropped, keys_a, vals_a, cell_start, prm, &ctr->bad_site);
   size_t bytes = cub_tmp_bytes;
   // counting sort (no radix passes); VX_RADIX_BIN=1: the stable radix sort
   static const bool radix_env = std::getenv("VX_RADIX_BIN") != nullptr;

@@ -757,7 +757,12 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
     for (int i = 0; i < 16; ++i) len.L[i] = i < d ? P->lengths[i] : 1.0;
     trace.rec(4, st);
     launches += launch_init(prm, ctr, st);
-    launches += launch_ingest(g, len, d, pos, times, weights, p3_copy, t_copy, ctr, st);
+    // device-pointer Voronoi calls in 3-D: the positions need no copy, so the
+    // binning pass itself checks them (one launch and one read of the sites
+    // fewer per call); host-buffer calls validate first (fail before any work)
+    const bool fuse_validation = !host_io && !use_brute && !use_nd && p3_alias && !timed(P);
+    if (fuse_validation) g.validate_in_keys = 1;
+    else launches += launch_ingest(g, len, d, pos, times, weights, p3_copy, t_copy, ctr, st);
     dbg(st, "ingest");
     if (host_io) {  // fail before any labelling work (SiteSet::validate)
       ck(cudaMemcpyAsync(&ctx->h_ctr->bad_site, &ctr->bad_site, sizeof(unsigned), cudaMemcpyDeviceToHost, st),
