@@ -321,9 +321,10 @@ def run_ours(args):
             # NCCL's communicator lines (rank count, NVLS / P2P transport) on
             # stderr, so the run's log shows the N it ran on; stdout keeps the
             # one JSON line
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+            if "NCCL_DEBUG" not in os.environ and os.access("/dev/stderr", os.W_OK):
+                os.environ["NCCL_DEBUG"] = "INFO"
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+                os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
             log(f"rank {rank}/{world}: NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}, "
                 f"device cuda:{dev} {torch.cuda.get_device_name(dev)}")

@@ -556,16 +556,21 @@ __global__ void __launch_bounds__(kUT)
     }
     double best = __longlong_as_double(0x7ff0000000000000ll);
     int bi = 0x7fffffff;
-    double rho = 2.0 * prm->gather_r;
+    // an unresolved voxel's nearest site lies just beyond the gather radius:
+    // start at 1.25 R and widen by 1.6
+    double rho = 1.25 * prm->gather_r;
+    if (!(rho > 0.0)) rho = g.lmax;
     for (int iter = 0; iter < 64; ++iter) {
       const bool last = rho * rho >= diag2;
       // cell box of [x - rho, x + rho] (whole axis when it wraps around)
       long long cl[kMaxDim], cr[kMaxDim], nrows = 1;
+      unsigned fullm = 0;  // bit a: the box covers the whole (periodic) axis
       for (int a = 0; a < D; ++a) {
         long long lo = (long long)floor((x[a] - rho) * g.inv_cw[a]) - 1, hi = (long long)floor((x[a] + rho) * g.inv_cw[a]) + 1;
         if (last || (PER && hi - lo + 1 >= g.m[a])) {
           lo = 0;
           hi = g.m[a] - 1;
+          fullm |= 1u << a;
         } else if (!PER) {
           lo = max(lo, 0ll);
           hi = min(hi, (long long)g.m[a] - 1);
@@ -580,14 +585,22 @@ __global__ void __launch_bounds__(kUT)
         int s0 = 0, s1 = 0;
         if (c < nrows) {
           long long rr = c, key = 0;
+          double d2 = 0.0;  // lower bound of the squared distance to the cell
           for (int a = 0; a < D; ++a) {
             long long cc = cl[a] + rr % cr[a];
             rr /= cr[a];
+            if (!((fullm >> a) & 1u)) {  // unwrapped cell index: its distance along a (a full axis adds 0)
+              const double gap = fmax(0.0, fmax(cc * g.cw[a] - x[a], x[a] - (cc + 1) * g.cw[a]));
+              d2 += gap * gap;
+            }
             if (PER) cc = wrapm(cc, g.m[a]);
             key += cc * g.cstride[a];
           }
-          s0 = bins.cell_start[key];
-          s1 = bins.cell_start[key + 1];
+          // every site of a cell farther than rho stays beyond the bound below
+          if (last || d2 <= rho * rho * (1.0 + 1e-6)) {
+            s0 = bins.cell_start[key];
+            s1 = bins.cell_start[key + 1];
+          }
         }
         for (int p = s0; p < s1; ++p) {
           double acc = 0.0;
@@ -619,7 +632,7 @@ __global__ void __launch_bounds__(kUT)
       if (KIND == kJohnsonMehl) bound = r1 / g.growth * (1.0 - 1e-9) + t_min - 1e-9 * fabs(t_min);
       if (KIND == kLaguerre) bound = r1 * r1 / g.growth * (1.0 - 1e-9) + t_min - 1e-9 * fabs(t_min);
       if (best < bound) break;  // strictly: a tie beyond rho could have a lower index
-      rho *= 2.0;
+      rho *= 1.6;
     }
     if (lane == 0) {
       labels[v] = bi;

@@ -48,15 +48,20 @@ for i in range(n_inst):
     lab_ref, dist_ref, _, _ = oracle.ref_tessellate(p, prune=prune, override=override)
     t_ref = time.time() - t0
     sites, grid = to_vx(p)
+    t1 = time.time()
     r = vx.tessellate_fast(sites, grid, vx.FastOptions(override_param=override, prune=prune), distances=True,
                            histogram=True)
+    t_ours = time.time() - t1
     ok_lab = bool(np.array_equal(r.labels.labels, lab_ref))
     ok_dist = bool(np.array_equal(r.distances.values.view(np.uint64), dist_ref.view(np.uint64)))
     ok_hist = bool(np.array_equal(r.histogram, np.bincount(lab_ref, minlength=ns).astype(np.uint64)))
     row = {"i": i, "d": d, "kind": kind, "periodic": periodic, "counts": counts, "n_sites": ns,
            "prune": prune, "override": override is not None, "labels": ok_lab, "values": ok_dist,
-           "histogram": ok_hist, "overflow_bricks": int(r.stats["overflow_bricks"]), "ref_s": round(t_ref, 3)}
+           "histogram": ok_hist, "overflow_bricks": int(r.stats["overflow_bricks"]), "ref_s": round(t_ref, 3),
+           "ours_s": round(t_ours, 3), "unresolved": int(r.stats["n_unresolved"])}
     rows.append(row)
+    if t_ours > 2.0:
+        print("SLOW", row, flush=True)
     if not (ok_lab and ok_dist and ok_hist):
         bad.append(row)
         print("MISMATCH", row, flush=True)
@@ -67,5 +72,5 @@ for dd in (1, 2, 3, 4):
     summary["by_dim"][dd] = sum(1 for r in rows if r["d"] == dd)
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 with open(os.path.join(ROOT, "gpurun_out", "parity_sweep.json"), "w") as f:
-    json.dump({"summary": summary, "bad": bad}, f, indent=1)
+    json.dump({"summary": summary, "bad": bad, "rows": rows}, f, indent=1)
 print(json.dumps(summary), flush=True)
