@@ -68,6 +68,12 @@ __device__ __forceinline__ long long wrapm(long long c, long long m) {
   return r < 0 ? r + m : r;
 }
 
+__device__ __forceinline__ long long slab_voxels(const GeoN& g, int D) {
+  long long n = g.ze - g.zb;
+  for (int a = 0; a < D - 1; ++a) n *= g.n[a];
+  return n;
+}
+
 // table column layout of a block: axis 0 (d = 1: none, d = 2: 16 columns,
 // d >= 4: 4), axis 1 (16 | 4), axes >= 2: E[a] columns each
 struct Layout {
@@ -191,6 +197,7 @@ __global__ void __launch_bounds__(32, 20)
           a0 = max(cx0, 0ll);
           a1 = min(cx1, mx - 1);
         }
+        VXCHK(base >= 0 && base + a1 + 1 <= g.n_cells && (c1 < c0 || base + c1 + 1 <= g.n_cells), "row cells");
         if (a1 >= a0) {
           st[0] = bins.cell_start[base + a0];
           cn[0] = bins.cell_start[base + a1 + 1] - st[0];
@@ -229,6 +236,7 @@ __global__ void __launch_bounds__(32, 20)
         }
         const int sg = ws.seg_off[2 * lo + 1] <= f ? 2 * lo + 1 : 2 * lo;
         p = ws.seg_start[sg] + (f - ws.seg_off[sg]);
+        VXCHK(p >= 0 && p < g.n_sites, "gathered position %d", p);
         double lb = 0.0, ub = 0.0;
         for (int a = 0; a < D; ++a) {
           double u = bins.x[p + a * bins.stride] - cc[a];
@@ -298,6 +306,7 @@ __global__ void __launch_bounds__(32, 20)
         const int4 v = key4[i];
         rank += (v.x < me) + (v.y < me) + (v.z < me) + (v.w < me);
       }
+      VXCHK(rank >= 0 && rank < nl && ws.u.a.lslot[k] < nk, "rank %d nl %d", rank, nl);
       ws.sp[rank] = ws.u.a.kp[ws.u.a.lslot[k]];
       ws.sidx[rank] = me;
       ws.cnt[rank] = 0;
@@ -393,6 +402,7 @@ __global__ void __launch_bounds__(32, 20)
     // exact tables: one lane per (candidate, axis)
     for (int e = lane; e < D * m; e += 32) {
       const int a = e / m, j = e - a * m;
+      VXCHK(Ly.off[a] + Ly.ext[a] <= kTW && j < kChunk, "table column %d", Ly.off[a] + Ly.ext[a]);
       const int p = ws.sp[c0 + j];
       const double sv = bins.x[p + a * bins.stride];
       const int ne = Ly.ext[a], col0 = Ly.off[a];
@@ -480,6 +490,7 @@ __global__ void __launch_bounds__(32, 20)
   for (int k = 0; k < 8; ++k) {
     if (!((vmask >> k) & 1u)) continue;
     const long long v = vox(k);
+    VXCHK(v >= 0 && v < slab_voxels(g, D), "voxel %lld", v);
     labels[v] = lab[k];
     if (dist && lab[k] >= 0) dist[v] = KIND == kVoronoi ? __dsqrt_rn(best[k]) : best[k];
   }
