@@ -213,7 +213,8 @@ __device__ __forceinline__ long long wrapi2(long long c, long long m) {
   return r < 0 ? r + m : r;
 }
 
-template <int KIND, bool PER, bool DENSE>
+// BL: standard lists per 8^3 brick (evaluated by eval16) instead of per 8 x 8 x 4 sub-brick
+template <int KIND, bool PER, bool DENSE, bool BL>
 __global__ void __launch_bounds__(kB2Threads, 4)
     cull12_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, int2* __restrict__ info,
                   int* __restrict__ slots16, int* __restrict__ list, long long list_cap,
@@ -591,10 +592,22 @@ __global__ void __launch_bounds__(kB2Threads, 4)
   }
   __syncwarp();
 
-  for (int q = 0; q < 2; ++q) {
+  // brick lists (standard lists only): one list per 8^3 brick instead of
+  // one per 8 x 8 x 4 sub-brick
+  constexpr bool BM = BL && !DENSE;
+  for (int q = 0; q < (BM ? 1 : 2); ++q) {
     const int sy = byo, sz = bzo + q * 4;
-    const int sext[3] = {bext[0], bext[1], min(4, ext[2] - sz)};
+    const int sext[3] = {bext[0], bext[1], min(BM ? 8 : 4, ext[2] - sz)};
     if (sext[1] <= 0 || sext[2] <= 0) continue;
+    // overflowed lists go to the sub-brick shell, 8 x 8 x 4 at a time
+    auto push_ovf = [&](void) {
+      ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz);
+      if (BM && sext[2] > 4) ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz + 4);
+    };
+    auto list_id = [&](void) -> long long {
+      return BM ? (long long)(bxo + K0[0]) / 8 + (long long)nsbx * ((K0[1] + sy) / 8 + nsby * ((K0[2] + sz - g.z_begin) >> 3))
+                : sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz);
+    };
     int n2 = 0;
     if (DENSE && brick_ok) {
       // two passes over the brick list in chunks of 32: arg-min of the upper
@@ -714,7 +727,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
                                                  bisector_keep<KIND, PER>(sb, flb, z, fl0, Bs, halfLf, invG, e_d)));
       // survivors -> the sub-brick's kSlot fixed slots (or the overflow
       // list when longer), in slot (= site index) order
-      const long long sbi = sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz);
+      const long long sbi = list_id();
       const unsigned ma = __ballot_sync(0xffffffffu, ka), mb = __ballot_sync(0xffffffffu, kb);
       n2 = __popc(ma) + __popc(mb);
       long long base = 0;
@@ -734,13 +747,12 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       }
       if (lane == 0) {
         info[sbi] = ok ? make_int2((int)base, n2) : make_int2(0, -1);
-        if (!ok) ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sbi;
+        if (!ok) push_ovf();
         if (ok && n2 <= kFcap) ws.evals += (unsigned)(n2 * sext[0] * sext[1] * sext[2]);
       }
     } else if (lane == 0) {
-      const long long sbi = sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz);
-      info[sbi] = make_int2(0, -1);
-      ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sbi;
+      info[list_id()] = make_int2(0, -1);
+      push_ovf();
     }
   }
   if (lane == 0 && !brick_ok) atomicAdd(&ctr->overflow_bricks, 1ull);
@@ -789,6 +801,9 @@ __device__ __forceinline__ void exact_tables(ES& ws, const Bins& bins, const Geo
 #endif
 constexpr int kEvalWarps = VX_EVAL_WARPS;  // sub-bricks along y per CTA
 constexpr unsigned kMaxGridY = 65535;      // gridDim.y limit: taller grids launch in y-chunks
+#ifndef VX_EVAL16_MINB
+#define VX_EVAL16_MINB 24  // 80 registers, no spills (20: 92 registers, 28: spills; cfg5 6.63 / 7.05 / 7.20 ms)
+#endif
 
 // One warp per 8x8x4 sub-brick (the tail of v11's sub-brick loop: exact
 // tables, evaluation, stores, histogram, unresolved compaction).  The site
@@ -996,6 +1011,185 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 32 / kEvalWarps)
   }
 }
 
+
+// eval16 (standard lists per 8^3 brick): one warp per brick, 16 voxels per
+// lane -- 4 along x in rows (vy, vy + 4) of planes (vz, vz + 4) -- so the x
+// table, the y-z sums and the per-brick setup are shared by twice the voxels
+// of eval12.  Same exact arithmetic, ascending-index strict-< scan, resolve,
+// stores, histogram and compaction.
+struct __align__(16) Eval16Smem {
+  double T[kFcap][24]; // exact w^2: [0,8) x, [8,16) y, [16,24) z
+  double C[24];
+  double Ft[kFcap];
+  int P[kFcap];
+  int Fidx[kFcap];
+  int cnt[kFcap];
+};
+
+template <int KIND, bool PER, bool FA>
+__global__ void __launch_bounds__(32, VX_EVAL16_MINB)
+    eval16_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, const int2* __restrict__ info,
+                  const int* __restrict__ slots16, const int* __restrict__ list, int* __restrict__ labels,
+                  double* __restrict__ dist, unsigned long long* __restrict__ hist, long long* __restrict__ unres,
+                  long long unres_cap, DevCounters* ctr, unsigned by0) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Eval16Smem& ws = *reinterpret_cast<Eval16Smem*>(smem_raw);
+  const int lane = threadIdx.x & 31;
+  const unsigned nsbx = g.nsbx, nsby = g.nsby;
+  const double cutoff = prm->cutoff;
+  const int qx = (lane & 1) * 4, vy = (lane >> 1) & 3, vz = lane >> 3;
+  const unsigned bx = blockIdx.x, by = by0 + blockIdx.y, bz = blockIdx.z;
+  if (by >= nsby) return;
+  const long long bi = (long long)bx + (long long)nsbx * ((long long)by + (long long)nsby * bz);
+  const int2 inf = info[bi];
+  const int ps = lane < kSlot ? slots16[bi * kSlot + lane] : 0;
+  const int pl = inf.y > kSlot ? (lane < inf.y ? list[inf.x + lane] : 0) : ps;
+  if (inf.y < 0) return;  // overflowed: the sub-brick shell labels it
+  const int x0 = (int)bx * 8, y0 = (int)by * 8;
+  const long long z0 = g.z_begin + (long long)bz * 8;
+  const int bext[3] = {min(8, (int)g.n[0] - x0), min(8, (int)g.n[1] - y0), (int)min(8ll, g.z_end - z0)};
+  const int n2 = inf.y <= kFcap ? inf.y : 0;  // longer lists: the per-voxel shell
+  int fidx = 0;
+  if (lane < n2) {
+    ws.P[lane] = pl;
+    ws.cnt[lane] = 0;
+    fidx = bins.idx[pl];
+    if (KIND != kVoronoi) ws.Ft[lane] = bins.t[pl];
+  }
+  if (lane < 24 && n2 > 0) {  // the brick's voxel centres (geometry.hpp:58-60)
+    const int a = lane >> 3;
+    const int k = min(lane & 7, (a == 0 ? bext[0] : (a == 1 ? bext[1] : bext[2])) - 1);
+    const long long k0 = a == 0 ? (long long)x0 : (a == 1 ? (long long)y0 : z0);
+    ws.C[lane] = center(k0 + k, a == 0 ? g.sp[0] : (a == 1 ? g.sp[1] : g.sp[2]));
+  }
+  __syncwarp();
+  // exact tables: one lane per (site, axis), 8 entries each
+  for (int e = lane; e < 3 * n2; e += 32) {
+    const int a = e >= 2 * n2 ? 2 : (e >= n2 ? 1 : 0);
+    const int j = e - a * n2;
+    const double sv = bins.x[ws.P[j] + a * bins.stride];
+    const double* cr = &ws.C[a * 8];
+    double u[8];
+    const double La = PER ? (a == 0 ? g.L[0] : (a == 1 ? g.L[1] : g.L[2])) : 0.0;
+    const double lim = 0.49 * La;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) u[r] = __dsub_rn(sv, cr[r]);
+    if (PER && (!(fabs(u[0]) < lim) || !(fabs(u[7]) < lim))) {
+      const double iLa = a == 0 ? g.invL[0] : (a == 1 ? g.invL[1] : g.invL[2]);
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (!(fabs(u[r]) < lim)) u[r] = wrap_delta(u[r], La, iLa);
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) ws.T[j][a * 8 + r] = __dmul_rn(u[r], u[r]);
+  }
+  if (lane < n2) ws.Fidx[lane] = fidx;
+  __syncwarp();
+  // voxel k = 8 zh + 4 yh + i: x = qx + i, y = vy + 4 yh, z = vz + 4 zh
+  double best[16];
+  int bj[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    best[k] = __longlong_as_double(0x7ff0000000000000ll);
+    bj[k] = 0;
+  }
+  const bool g1 = g.g_is_one;
+  for (int j = 0; j < n2; ++j) {
+    const double wz0 = ws.T[j][16 + vz], wz1 = ws.T[j][20 + vz];
+    const double wy0 = ws.T[j][8 + vy], wy1 = ws.T[j][12 + vy];
+    const double a[4] = {__dadd_rn(wz0, wy0), __dadd_rn(wz0, wy1), __dadd_rn(wz1, wy0), __dadd_rn(wz1, wy1)};
+    const double2 w01 = *reinterpret_cast<const double2*>(&ws.T[j][qx]);
+    const double2 w23 = *reinterpret_cast<const double2*>(&ws.T[j][qx + 2]);
+    const double wx[4] = {w01.x, w01.y, w23.x, w23.y};
+    const double tj = KIND == kVoronoi ? 0.0 : ws.Ft[j];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double d = __dadd_rn(a[r], wx[i]);
+        const double pr = FA ? prox_from_dsq_nc<KIND>(d, g.growth, g1, tj, g.inv_growth_rn)
+                             : prox_from_dsq<KIND>(d, g.growth, g1, tj);
+        const int k = 4 * r + i;  // r = 2 zh + yh
+        if (pr < best[k]) {
+          best[k] = pr;
+          bj[k] = j;
+        }
+      }
+    }
+  }
+  // ---- resolve + store + compaction ----
+  const int xr = bext[0] - qx;
+  const unsigned xm = xr >= 4 ? 0xFu : (xr > 0 ? (1u << xr) - 1u : 0u);
+  unsigned vmask = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int yy = vy + 4 * (r & 1), zz = vz + 4 * (r >> 1);
+    if (yy < bext[1] && zz < bext[2]) vmask |= xm << (4 * r);
+  }
+  int lab[16];
+  unsigned umask = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    lab[k] = -1;
+    if ((vmask >> k) & 1u) {
+      if (best[k] <= cutoff) {
+        lab[k] = ws.Fidx[bj[k]];
+        if (hist) atomicAdd(&ws.cnt[bj[k]], 1);
+      } else {
+        umask |= 1u << k;
+      }
+    }
+  }
+  const long long slab_z = (long long)bz * 8 + vz;  // z inside the slab
+  auto vox = [&](int r) -> long long {
+    return (slab_z + 4 * (r >> 1)) * g.plane + (long long)(y0 + vy + 4 * (r & 1)) * g.n[0] + x0 + qx;
+  };
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    if (!((vmask >> (4 * r)) & 0xFu)) continue;
+    int* out = labels + vox(r);
+    if (xm == 0xFu && g.vec_store) {
+      *reinterpret_cast<int4*>(out) = make_int4(lab[4 * r], lab[4 * r + 1], lab[4 * r + 2], lab[4 * r + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if ((xm >> i) & 1u) out[i] = lab[4 * r + i];
+    }
+    if (dist) {
+      double* dout = dist + vox(r);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (((xm >> i) & 1u) && lab[4 * r + i] >= 0)
+          dout[i] = KIND == kVoronoi ? __dsqrt_rn(best[4 * r + i]) : best[4 * r + i];
+    }
+  }
+  if (__any_sync(0xffffffffu, umask != 0)) {
+    const int nun = __popc(umask);
+    int inc = nun;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int wtot = __shfl_sync(0xffffffffu, inc, 31);
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(&ctr->n_unres, (unsigned long long)wtot);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    const long long off = (long long)base + inc - nun;
+    unsigned mm = umask;
+    for (int i = 0; i < nun; ++i) {
+      const int k = __ffs(mm) - 1;
+      mm &= mm - 1;
+      if (off + i < unres_cap) unres[off + i] = g.z_begin * g.plane + vox(k >> 2) + (k & 3);
+    }
+  }
+  if (hist && n2 > 0) {
+    __syncwarp();
+    for (int i = lane; i < n2; i += 32)
+      if (ws.cnt[i]) atomicAdd(&hist[ws.Fidx[i]], (unsigned long long)ws.cnt[i]);
+  }
+}
+
 }  // namespace v12
 
 __global__ void ball12_publish_kernel(const unsigned long long* slots, DevCounters* ctr) {
@@ -1073,8 +1267,15 @@ static int launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* l
   const bool attr = (attr_done.load() & bit) != 0;
   const size_t sh_c = sizeof(v12::Smem2);
   const size_t sh_e = sizeof(v12::EvalSmemT<DENSE ? v12::kLcapD : v12::kFcap>) * v12::kEvalWarps;
+  // brick lists + eval16 for Voronoi and Laguerre (JM keeps sub-brick lists:
+  // its in-loop sqrt needs the registers eval16 spends on 16 voxels per lane)
+  static const bool sub_env = std::getenv("VX_SUBBRICK_LISTS") != nullptr;
+  const bool bl = !DENSE && KIND != kJohnsonMehl && !sub_env;
   if (!attr) {
-    cudaFuncSetAttribute(v12::cull12_kernel<KIND, PER, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_c);
+    cudaFuncSetAttribute(v12::cull12_kernel<KIND, PER, DENSE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sh_c);
+    cudaFuncSetAttribute(v12::cull12_kernel<KIND, PER, DENSE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sh_c);
     cudaFuncSetAttribute(v12::eval12_kernel<KIND, PER, DENSE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_e);
     if (KIND != kVoronoi)
       cudaFuncSetAttribute(v12::eval12_kernel<KIND, PER, DENSE, KIND != kVoronoi>,
@@ -1088,10 +1289,35 @@ static int launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* l
     const dim3 grid((unsigned)((g.n[0] + v12::kSB - 1) / v12::kSB),
                     (unsigned)std::min<long long>(v12::kMaxGridY, sbrows - y0),
                     (unsigned)((g.z_end - g.z_begin + 16 * nbb - 1) / (16 * nbb)));
-    v12::cull12_kernel<KIND, PER, DENSE><<<grid, v12::kB2Threads, sh_c, st>>>(
-        g, bins, prm, info, slots16, list, list_cap, list_count, ovf, ctr, slots, nbb, (unsigned)y0);
+    if (bl)
+      v12::cull12_kernel<KIND, PER, DENSE, true><<<grid, v12::kB2Threads, sh_c, st>>>(
+          g, bins, prm, info, slots16, list, list_cap, list_count, ovf, ctr, slots, nbb, (unsigned)y0);
+    else
+      v12::cull12_kernel<KIND, PER, DENSE, false><<<grid, v12::kB2Threads, sh_c, st>>>(
+          g, bins, prm, info, slots16, list, list_cap, list_count, ovf, ctr, slots, nbb, (unsigned)y0);
   }
   const long long nsb = ball12_subbricks(g);
+  if constexpr (KIND != kJohnsonMehl) if (bl) {
+    const size_t sh16 = sizeof(v12::Eval16Smem);
+    if (!attr) {
+      cudaFuncSetAttribute(v12::eval16_kernel<KIND, PER, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh16);
+      cudaFuncSetAttribute(v12::eval16_kernel<KIND, PER, KIND != kVoronoi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sh16);
+    }
+    const long long brows = (g.n[1] + 7) / 8;
+    for (long long r0 = 0; r0 < brows; r0 += v12::kMaxGridY, ++launches) {
+      const dim3 eg((unsigned)((g.n[0] + 7) / 8), (unsigned)std::min<long long>(v12::kMaxGridY, brows - r0),
+                    (unsigned)((g.z_end - g.z_begin + 7) / 8));
+      if (KIND != kVoronoi && g.fast_arith)
+        v12::eval16_kernel<KIND, PER, KIND != kVoronoi><<<eg, 32, sh16, st>>>(g, bins, prm, info, slots16, list, labels, dist,
+                                                                              hist, unres, cap, ctr, (unsigned)r0);
+      else
+        v12::eval16_kernel<KIND, PER, false><<<eg, 32, sh16, st>>>(g, bins, prm, info, slots16, list, labels, dist, hist,
+                                                                   unres, cap, ctr, (unsigned)r0);
+    }
+    launch_subshell(g, bins, prm, ovf, &ctr->n_ovf_sb, labels, dist, hist, ctr, st);
+    return launches - 2;
+  }
   const long long rows = ((g.n[1] + 7) / 8 + v12::kEvalWarps - 1) / v12::kEvalWarps;  // CTA rows along y
   for (long long r0 = 0; r0 < rows; r0 += v12::kMaxGridY, ++launches) {
     const dim3 eg((unsigned)((g.n[0] + 7) / 8), (unsigned)std::min<long long>(v12::kMaxGridY, rows - r0),
