@@ -75,6 +75,7 @@ struct __align__(16) WarpSmem {
   int L[kLcapD];       // dense mode: a sub-brick's survivors (binned positions)
   float4 bxy;          // the column's x/y box (c[0], c[1], h[0], h[1]), shared by its sub-bricks
   unsigned evals;      // exact evaluations the eval kernel will do for this warp's sub-bricks
+  alignas(16) float zref2[16]; // the second reference (VX_TWO_REFS)
   alignas(16) float zref[16];  // the sub-brick's reference site: SiteF fields + flags (written by its lane)
 };
 
@@ -721,10 +722,51 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       }
       const float tau = fminf(z.ubp, tcf);
       const unsigned fl0 = __float_as_uint(ws.zref[13]);
-      const bool ka = va && (lane == r0 || (sa.lbp <= tau &&
+      bool ka, kb;
+      if constexpr (KIND == kVoronoi && BM) {
+      // Voronoi brick lists: a second reference, the next-least upper bound
+      // (cfg2 -2.4 %, cfg5 -1.6 %; JM / Laguerre spill with it)
+      unsigned km2 = min(va && lane != r0 ? ((okey(sa.ubp) & ~63u) | (unsigned)lane) : 0xffffffffu,
+                         vb && lane + 32 != r0 ? ((okey(sb.ubp) & ~63u) | (unsigned)(lane + 32)) : 0xffffffffu);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) km2 = min(km2, __shfl_xor_sync(0xffffffffu, km2, o));
+      const bool two = km2 != 0xffffffffu;
+      const int r1 = (int)(km2 & 63u), rl1 = r1 & 31;
+      const bool rhi1 = r1 >= 32;
+      if (two && lane == rl1) {
+        const SiteF& o = rhi1 ? sb : sa;
+        float* zr = ws.zref2;
+        zr[0] = o.v[0], zr[1] = o.v[1], zr[2] = o.v[2];
+        zr[3] = o.mn[0], zr[4] = o.mn[1], zr[5] = o.mn[2];
+        zr[6] = o.mx[0], zr[7] = o.mx[1], zr[8] = o.mx[2];
+        zr[9] = o.t, zr[10] = o.lb, zr[11] = o.ub, zr[12] = o.ubp;
+        zr[13] = __uint_as_float(rhi1 ? flb : fla);
+      }
+      __syncwarp();
+      auto keep2 = [&](const SiteF& sx, unsigned flx, int slot) {
+        if (!two || slot == r1) return true;
+        SiteF z2;
+        const float4 q0 = *reinterpret_cast<const float4*>(&ws.zref2[0]);
+        const float4 q1 = *reinterpret_cast<const float4*>(&ws.zref2[4]);
+        const float4 q2 = *reinterpret_cast<const float4*>(&ws.zref2[8]);
+        z2.v[0] = q0.x, z2.v[1] = q0.y, z2.v[2] = q0.z;
+        z2.mn[0] = q0.w, z2.mn[1] = q1.x, z2.mn[2] = q1.y;
+        z2.mx[0] = q1.z, z2.mx[1] = q1.w, z2.mx[2] = q2.x;
+        z2.t = q2.y, z2.lb = q2.z, z2.ub = q2.w;
+        return bisector_keep<KIND, PER>(sx, flx, z2, __float_as_uint(ws.zref2[13]), Bs, halfLf, invG, e_d);
+      };
+      ka = va && (lane == r0 || (sa.lbp <= tau &&
+                                            bisector_keep<KIND, PER>(sa, fla, z, fl0, Bs, halfLf, invG, e_d) &&
+                                            keep2(sa, fla, lane)));
+      kb = vb && (lane + 32 == r0 || (sb.lbp <= tau &&
+                                                 bisector_keep<KIND, PER>(sb, flb, z, fl0, Bs, halfLf, invG, e_d) &&
+                                                 keep2(sb, flb, lane + 32)));
+      } else {
+      ka = va && (lane == r0 || (sa.lbp <= tau &&
                                             bisector_keep<KIND, PER>(sa, fla, z, fl0, Bs, halfLf, invG, e_d)));
-      const bool kb = vb && (lane + 32 == r0 || (sb.lbp <= tau &&
+      kb = vb && (lane + 32 == r0 || (sb.lbp <= tau &&
                                                  bisector_keep<KIND, PER>(sb, flb, z, fl0, Bs, halfLf, invG, e_d)));
+      }
       // survivors -> the sub-brick's kSlot fixed slots (or the overflow
       // list when longer), in slot (= site index) order
       const long long sbi = list_id();
