@@ -37,6 +37,7 @@
 // Split at the sub-brick lists, both kernels fit 64 registers and run at 4
 // CTAs/SM; the lists cost ~0.7 GB of HBM traffic at cfg5.
 #include <algorithm>
+#include <type_traits>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -920,18 +921,24 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 32 / kEvalWarps)
     const unsigned vmask = vz < sext[2] ? ((vy < sext[1] ? xm : 0u) | (vy + 4 < sext[1] ? xm << 4 : 0u)) : 0u;
     int lab[8];
     unsigned umask = 0;  // bit k: voxel k valid but unresolved
+    // sub-bricks entirely inside the grid skip the per-voxel validity tests
+    auto resolve = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      lab[k] = -1;
-      if ((vmask >> k) & 1u) {
-        if (best[k] <= cutoff) {  // best = +inf when there is no candidate
-          lab[k] = ws.Fidx[bj[k]];
-          if (hist) atomicAdd(&ws.cnt[bj[k]], 1);
-        } else {
-          umask |= 1u << k;
+      for (int k = 0; k < 8; ++k) {
+        lab[k] = -1;
+        if (FULL || ((vmask >> k) & 1u)) {
+          if (best[k] <= cutoff) {  // best = +inf when there is no candidate
+            lab[k] = ws.Fidx[bj[k]];
+            if (hist) atomicAdd(&ws.cnt[bj[k]], 1);
+          } else {
+            umask |= 1u << k;
+          }
         }
       }
-    }
+    };
+    if (vmask == 0xFFu) resolve(std::true_type{});
+    else resolve(std::false_type{});
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (!((vmask >> (4 * h)) & 0xFu)) continue;
@@ -1170,18 +1177,25 @@ __global__ void __launch_bounds__(32, VX_EVAL16_MINB)
   }
   int lab[16];
   unsigned umask = 0;
+  // bricks entirely inside the grid (all but the boundary layers) skip the
+  // per-voxel validity tests
+  auto resolve = [&](auto full_tag) {
+    constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    lab[k] = -1;
-    if ((vmask >> k) & 1u) {
-      if (best[k] <= cutoff) {
-        lab[k] = ws.Fidx[bj[k]];
-        if (hist) atomicAdd(&ws.cnt[bj[k]], 1);
-      } else {
-        umask |= 1u << k;
+    for (int k = 0; k < 16; ++k) {
+      lab[k] = -1;
+      if (FULL || ((vmask >> k) & 1u)) {
+        if (best[k] <= cutoff) {
+          lab[k] = ws.Fidx[bj[k]];
+          if (hist) atomicAdd(&ws.cnt[bj[k]], 1);
+        } else {
+          umask |= 1u << k;
+        }
       }
     }
-  }
+  };
+  if (vmask == 0xFFFFu) resolve(std::true_type{});
+  else resolve(std::false_type{});
   const long long slab_z = (long long)bz * 8 + vz;  // z inside the slab
   auto vox = [&](int r) -> long long {
     return (slab_z + 4 * (r >> 1)) * g.plane + (long long)(y0 + vy + 4 * (r & 1)) * g.n[0] + x0 + qx;
