@@ -1197,14 +1197,16 @@ __global__ void __launch_bounds__(32, VX_EVAL16_MINB)
   if (vmask == 0xFFFFu) resolve(std::true_type{});
   else resolve(std::false_type{});
   const long long slab_z = (long long)bz * 8 + vz;  // z inside the slab
-  auto vox = [&](int r) -> long long {
-    return (slab_z + 4 * (r >> 1)) * g.plane + (long long)(y0 + vy + 4 * (r & 1)) * g.n[0] + x0 + qx;
-  };
+  // row r = 2 zh + yh: voxel offset of its first x, rows 4 planes / 4 rows apart
+  const long long vox0 = slab_z * g.plane + (long long)(y0 + vy) * g.n[0] + x0 + qx;
+  const long long ystep = 4 * g.n[0], zstep = 4 * g.plane;
+  auto vox = [&](int r) -> long long { return vox0 + (r >> 1) * zstep + (r & 1) * ystep; };
+  const bool full = vmask == 0xFFFFu;
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
-    if (!((vmask >> (4 * r)) & 0xFu)) continue;
+    if (!full && !((vmask >> (4 * r)) & 0xFu)) continue;
     int* out = labels + vox(r);
-    if (xm == 0xFu && g.vec_store) {
+    if ((full || xm == 0xFu) && g.vec_store) {
       *reinterpret_cast<int4*>(out) = make_int4(lab[4 * r], lab[4 * r + 1], lab[4 * r + 2], lab[4 * r + 3]);
     } else {
 #pragma unroll
