@@ -8,7 +8,6 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 timeout 900 python scripts/configs_table.py $T > gpurun_out/configs_$T.log 2>&1
 timeout 900 python scripts/nd_quick.py 0 11 --time > gpurun_out/nd_engine_$T.txt 2>&1
 timeout 600 python scripts/slab_scaling.py > gpurun_out/slab_scaling_$T.txt 2>&1
-timeout 1200 python scripts/parity_sweep.py 300 > gpurun_out/parity_sweep_$T.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_cfg5_$T.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_launch_$T.log 2>&1
 REPS=1 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"cull12|eval12|eval16" -c 2 -f -o gpurun_out/ball12_cfg5_$T python scripts/ab_time.py 5 > gpurun_out/ncu_full_$T.log 2>&1
 echo done
