@@ -65,6 +65,14 @@ constexpr int kLcapD = 128;
 constexpr int kSlot = 16;         // fixed list slots per sub-brick (longer lists: overflow list)
 constexpr int kRows2 = 256;       // cell rows per super-brick
 constexpr float kRel = 1e-5f;
+#ifndef VX_COL_OLD
+#define VX_COL_OLD 0
+#endif
+// the gathered sites are moved into site-index order after the rank sort
+// (instead of an index permutation read by every brick's list pass)
+#ifndef VX_PERMUTE
+#define VX_PERMUTE 1
+#endif
 
 struct FBox {
   float c[3];  // centre relative to the super-brick centre
@@ -105,7 +113,14 @@ struct Smem2 {
   int n_total;
   int n_kept;
   double cx[kSB], cy[kSB], cz[kSZ];  // exact voxel centres of the super-brick
-  WarpSmem w[kB2Threads / 32];
+  union {
+    WarpSmem w[kB2Threads / 32];
+    struct {  // VX_PERMUTE: the gather's staging arrays (dead once the sites are in order)
+      float4 rel[kTcap];
+      int p[kTcap];
+      unsigned char flag[kTcap];
+    } g;
+  };
 };
 
 __device__ __forceinline__ float lo_add(float a, float b) {
@@ -164,32 +179,64 @@ __device__ __forceinline__ void fbounds(const float4 s, unsigned flags, const FB
   }
 }
 
+// The reference-site terms of bisector_keep, once per box: Z2 = |z|^2 and
+// Kz = sum_a (|z_a| + 2 h_a) + 3 e_d.
+__device__ __forceinline__ void ref_consts(const SiteF& z, const FBox& B, float e_d, float& Z2, float& Kz) {
+  Z2 = 0.f;
+  Kz = 3.f * e_d;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    Z2 = __fmaf_rn(z.v[a], z.v[a], Z2);
+    Kz += fabsf(z.v[a]) + 2.f * B.h[a];
+  }
+}
+
 // true iff s may beat (or tie) s0 somewhere in B: lower bound of prox_s - prox_s0 <= 0.
+// min over x in B of |s - x|^2 - |z - x|^2 = sum_a s_a^2 - z_a^2 - 2 h_a |s_a - z_a|
+// (x relative to the box centre); f32 rounding of the sums is covered by
+// kRel x their magnitude, and the f32 coordinates' own error (|err| <= e_d
+// per coordinate, e_d >= 16x the rounding of the relative coordinates) by
+// pert = 2 e_d sum_a (|s_a| + |z_a| + 2 h_a + e_d), subtracted in full.
 template <int KIND, bool PER>
 __device__ __forceinline__ bool bisector_keep(const SiteF& s, unsigned fs, const SiteF& z,
                                               unsigned f0, const FBox& B, const float* halfL,
-                                              float invG, float e_d) {
-  float D = 0.f, mag = 0.f;
+                                              float invG, float e_d, float Z2, float Kz) {
+  float D, mag, pert;
   // neither site near half a period (flag bits 3..5): no axis needs the wrap bound
   const bool anyrisk = PER && ((fs | f0) & 0x38u) != 0u;
+  if (!anyrisk) {
+    float S2 = 0.f, Hs = 0.f, As = 0.f;
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const bool wrapcase = anyrisk && (((fs | f0) >> a) & 1u ||
-                                      fabsf(s.v[a]) + B.h[a] > halfL[a] * (1.f - 1e-5f) ||
-                                      fabsf(z.v[a]) + B.h[a] > halfL[a] * (1.f - 1e-5f));
-    float term, m;
-    if (wrapcase) {
-      term = s.mn[a] * s.mn[a] - z.mx[a] * z.mx[a];
-      m = s.mn[a] * s.mn[a] + z.mx[a] * z.mx[a];
-    } else {
+    for (int a = 0; a < 3; ++a) {
       const float dv = fabsf(s.v[a] - z.v[a]);
-      term = s.v[a] * s.v[a] - z.v[a] * z.v[a] - 2.f * B.h[a] * dv;
-      m = s.v[a] * s.v[a] + z.v[a] * z.v[a] + 2.f * B.h[a] * dv;
+      S2 = __fmaf_rn(s.v[a], s.v[a], S2);
+      Hs = __fmaf_rn(2.f * B.h[a], dv, Hs);
+      As += fabsf(s.v[a]);
     }
-    D += term;
-    mag += m + 2.f * e_d * (fabsf(s.v[a]) + fabsf(z.v[a]) + 2.f * B.h[a] + e_d);
+    D = (S2 - Z2) - Hs;
+    mag = (S2 + Z2) + Hs;
+    pert = 2.f * e_d * (As + Kz);
+  } else {
+    D = 0.f, mag = 0.f, pert = 0.f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const bool wrapcase = ((fs | f0) >> a) & 1u || fabsf(s.v[a]) + B.h[a] > halfL[a] * (1.f - 1e-5f) ||
+                            fabsf(z.v[a]) + B.h[a] > halfL[a] * (1.f - 1e-5f);
+      float term, m;
+      if (wrapcase) {
+        term = s.mn[a] * s.mn[a] - z.mx[a] * z.mx[a];
+        m = s.mn[a] * s.mn[a] + z.mx[a] * z.mx[a];
+      } else {
+        const float dv = fabsf(s.v[a] - z.v[a]);
+        term = s.v[a] * s.v[a] - z.v[a] * z.v[a] - 2.f * B.h[a] * dv;
+        m = s.v[a] * s.v[a] + z.v[a] * z.v[a] + 2.f * B.h[a] * dv;
+      }
+      D += term;
+      mag += m;
+      pert += 2.f * e_d * (fabsf(s.v[a]) + fabsf(z.v[a]) + 2.f * B.h[a] + e_d);
+    }
   }
-  const float Dlo = D - kRel * mag;  // lower bound of min_B (d_s^2 - d_s0^2)
+  const float Dlo = D - kRel * mag - pert;  // lower bound of min_B (d_s^2 - d_s0^2)
   if (KIND == kVoronoi) return Dlo <= 0.f;
   const float dt = lo_add(s.t - kRel * fabsf(s.t), -(z.t + kRel * fabsf(z.t)));
   if (KIND == kLaguerre) {
@@ -418,10 +465,16 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       base = __shfl_sync(0xffffffffu, base, 0);
       const int pos = base + __popc(m & ((1u << lane) - 1u));
       if (keep && pos < kTcap) {
+#if VX_PERMUTE
+        S.g.rel[pos] = make_float4(uf[0], uf[1], uf[2], (float)tv);
+        S.g.p[pos] = p;
+        S.g.flag[pos] = (unsigned char)fl;
+#else
         S.rel[pos] = make_float4(uf[0], uf[1], uf[2], (float)tv);
         S.p[pos] = p;
-        S.idx[pos] = bins.idx[p];
         S.flag[pos] = (unsigned char)fl;
+#endif
+        S.idx[pos] = bins.idx[p];
       }
     }
   }
@@ -431,12 +484,30 @@ __global__ void __launch_bounds__(kB2Threads, 4)
     for (int f = tid; f < T; f += kB2Threads) {
       const int me = S.idx[f];
       const int4* idx4 = reinterpret_cast<const int4*>(S.idx);  // padded with INT_MAX
-      int rank = 0;
-      for (int k = 0; k < (T + 3) >> 2; ++k) {
+      // the carry of v - me (v + ~me + 1) is set iff v >= me: a carry chain
+      // counts them at 1.5 instructions per comparison (ptxas pairs two carries
+      // per IADD3.X); rank = the padded count minus that
+      const int nk = (T + 3) >> 2;
+      unsigned ge = 0;
+      for (int k = 0; k < nk; ++k) {
         const int4 v = idx4[k];
-        rank += (v.x < me) + (v.y < me) + (v.z < me) + (v.w < me);
+        unsigned t;
+        asm("sub.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %1, 0;\n\t"
+            "sub.cc.u32 %0, %4, %3;\n\taddc.u32 %1, %1, 0;\n\t"
+            "sub.cc.u32 %0, %5, %3;\n\taddc.u32 %1, %1, 0;\n\t"
+            "sub.cc.u32 %0, %6, %3;\n\taddc.u32 %1, %1, 0;"
+            : "=&r"(t), "+r"(ge)
+            : "r"(v.x), "r"(me), "r"(v.y), "r"(v.z), "r"(v.w));
       }
+      const unsigned rank = 4u * (unsigned)nk - ge;
+      VXCHK(rank < (unsigned)T);
+#if VX_PERMUTE
+      S.rel[rank] = S.g.rel[f];
+      S.p[rank] = S.g.p[f];
+      S.flag[rank] = S.g.flag[f];
+#else
       S.ord[rank] = (short)f;
+#endif
     }
   }
   __syncthreads();
@@ -511,6 +582,85 @@ __global__ void __launch_bounds__(kB2Threads, 4)
   };
   if (!col_any) return;  // no barrier follows
   if (cta_ok) {
+#if !VX_COL_OLD
+    // Column passes.  A periodic-ambiguous axis (flag bit a) is fed in as a
+    // NaN coordinate: fminf(NaN, L/2) = L/2 (the upper bound's cap) and
+    // fmaxf(NaN, 0) = 0 (the lower bound's), so no per-brick flag test.  For
+    // Voronoi the (1 + kRel) widening commutes with the minimum (RN(x c) is
+    // monotone in x) and the lower-bound test lb (1 - kRel) <= tau is replaced
+    // by the weaker lb <= tau / (1 - kRel) (1 + 1e-6): a superset is kept.
+    const float qnan = __int_as_float(0x7fffffff);
+    float myub[kMaxBB];
+#pragma unroll
+    for (int b = 0; b < kMaxBB; ++b) myub[b] = __int_as_float(0x7f800000);
+    // full columns (nbb = kMaxBB, the common case) without per-brick count tests
+    auto pass1 = [&](auto nb_tag) {
+    constexpr int NB = decltype(nb_tag)::value;
+    for (int f = lane; f < T; f += 32) {
+      const float4 s = S.rel[f];
+      const unsigned fl = PER ? S.flag[f] : 0u;
+      const float sx = PER && (fl & 1u) ? qnan : s.x;
+      const float sy = PER && (fl & 2u) ? qnan : s.y;
+      const float sz = PER && (fl & 4u) ? qnan : s.z;
+      float mx = fabsf(sx - Bxy.c[0]) + Bxy.h[0];
+      float my = fabsf(sy - Bxy.c[1]) + Bxy.h[1];
+      if (PER) {
+        mx = fminf(mx, halfLf[0]);
+        my = fminf(my, halfLf[1]);
+      }
+      const float bxy = __fmaf_rn(my, my, mx * mx);
+#pragma unroll
+      for (int b = 0; b < kMaxBB; ++b) {
+        if (NB == 0 && b >= nbb) break;
+        float mz = fabsf(sz - bzc[b]) + bzh[b];
+        if (PER) mz = fminf(mz, halfLf[2]);
+        const float u2 = __fmaf_rn(mz, mz, bxy);
+        myub[b] = fminf(myub[b], KIND == kVoronoi ? u2
+                                                  : hi_add((KIND == kJohnsonMehl ? sqrtf(u2 * (1.f + kRel)) : u2 * (1.f + kRel)) * invG * (1.f + kRel),
+                                                           s.w + kRel * fabsf(s.w)));
+      }
+    }
+    };
+    if (nbb == kMaxBB) pass1(std::integral_constant<int, kMaxBB>{});
+    else pass1(std::integral_constant<int, 0>{});
+    float tlb[kMaxBB];  // Voronoi: the lower-bound threshold
+#pragma unroll
+    for (int b = 0; b < kMaxBB; ++b) {
+      float t = myub[b];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t = fminf(t, __shfl_xor_sync(0xffffffffu, t, o));
+      if (KIND == kVoronoi) t *= 1.f + kRel;
+      tau[b] = bval[b] ? fminf(t, tcf) : __int_as_float(0xff800000);  // -inf: keeps nothing
+      tlb[b] = KIND == kVoronoi ? tau[b] * ((1.f + 1e-6f) / (1.f - kRel)) : tau[b];
+    }
+    auto pass2 = [&](auto nb_tag) {
+    constexpr int NB = decltype(nb_tag)::value;
+    for (int f = lane; f < T; f += 32) {
+      const float4 s = S.rel[f];
+      const unsigned fl = PER ? S.flag[f] : 0u;
+      const float sx = PER && (fl & 1u) ? qnan : s.x;
+      const float sy = PER && (fl & 2u) ? qnan : s.y;
+      const float sz = PER && (fl & 4u) ? qnan : s.z;
+      const float lx = fmaxf(fabsf(sx - Bxy.c[0]) - Bxy.h[0], 0.f);
+      const float ly = fmaxf(fabsf(sy - Bxy.c[1]) - Bxy.h[1], 0.f);
+      const float bxy = __fmaf_rn(ly, ly, lx * lx);
+      unsigned m = 0;
+#pragma unroll
+      for (int b = 0; b < kMaxBB; ++b) {
+        if (NB == 0 && b >= nbb) break;
+        const float lz = fmaxf(fabsf(sz - bzc[b]) - bzh[b], 0.f);
+        const float l2 = __fmaf_rn(lz, lz, bxy);
+        const float lbp = KIND == kVoronoi ? l2
+                                           : lo_add((KIND == kJohnsonMehl ? sqrtf(l2 * (1.f - kRel)) : l2 * (1.f - kRel)) * invG * (1.f - kRel),
+                                                    s.w - kRel * fabsf(s.w));
+        if (lbp <= tlb[b]) m |= 1u << b;
+      }
+      S.mk[wid][f] = (unsigned char)m;
+    }
+    };
+    if (nbb == kMaxBB) pass2(std::integral_constant<int, kMaxBB>{});
+    else pass2(std::integral_constant<int, 0>{});
+#else
     float myub[kMaxBB];
 #pragma unroll
     for (int b = 0; b < kMaxBB; ++b) myub[b] = __int_as_float(0x7f800000);
@@ -566,6 +716,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       }
       S.mk[wid][f] = (unsigned char)m;
     }
+#endif
     __syncwarp();
   }
 
@@ -578,7 +729,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
   bool brick_ok = lists_ok;
   if (brick_ok) {
     for (int f0 = 0; f0 < T; f0 += 32) {
-      const int f = f0 + lane < T ? S.ord[f0 + lane] : 0;
+      const int f = f0 + lane < T ? (VX_PERMUTE ? f0 + lane : S.ord[f0 + lane]) : 0;
       const bool keep = f0 + lane < T && ((S.mk[wid][f] >> bb) & 1u);
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       const int pos = nW + __popc(m & ((1u << lane) - 1u));
@@ -637,6 +788,8 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       const unsigned fl0 = S.flag[fr];
       SiteF z;  // every lane derives the reference's bounds itself
       fbounds<KIND, PER>(S.rel[fr], fl0, Bs, halfLf, invG, z);
+      float zZ2, zKz;
+      ref_consts(z, Bs, e_d, zZ2, zKz);
       const float tau = fminf(z.ubp, tcf);  // >= the minimum upper bound: a valid cull level
       for (int c0 = 0; c0 < nW; c0 += 32) {
         const int k = c0 + lane;
@@ -647,7 +800,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
           const unsigned fl = S.flag[f];
           SiteF t;
           fbounds<KIND, PER>(S.rel[f], fl, Bs, halfLf, invG, t);
-          keep = k == r0 || (t.lbp <= tau && bisector_keep<KIND, PER>(t, fl, z, fl0, Bs, halfLf, invG, e_d));
+          keep = k == r0 || (t.lbp <= tau && bisector_keep<KIND, PER>(t, fl, z, fl0, Bs, halfLf, invG, e_d, zZ2, zKz));
         }
         const unsigned m = __ballot_sync(0xffffffffu, keep);
         const int pos = n2 + __popc(m & ((1u << lane) - 1u));
@@ -707,14 +860,16 @@ __global__ void __launch_bounds__(kB2Threads, 4)
         zr[6] = o.mx[0], zr[7] = o.mx[1], zr[8] = o.mx[2];
         zr[9] = o.t, zr[10] = o.lb, zr[11] = o.ub, zr[12] = o.ubp;
         zr[13] = __uint_as_float(rhi ? flb : fla);
+        ref_consts(o, Bs, e_d, zr[14], zr[15]);
       }
       __syncwarp();
       SiteF z;
+      float4 q3;
       {
         const float4 q0 = *reinterpret_cast<const float4*>(&ws.zref[0]);
         const float4 q1 = *reinterpret_cast<const float4*>(&ws.zref[4]);
         const float4 q2 = *reinterpret_cast<const float4*>(&ws.zref[8]);
-        const float2 q3 = *reinterpret_cast<const float2*>(&ws.zref[12]);
+        q3 = *reinterpret_cast<const float4*>(&ws.zref[12]);
         z.v[0] = q0.x, z.v[1] = q0.y, z.v[2] = q0.z;
         z.mn[0] = q0.w, z.mn[1] = q1.x, z.mn[2] = q1.y;
         z.mx[0] = q1.z, z.mx[1] = q1.w, z.mx[2] = q2.x;
@@ -722,7 +877,8 @@ __global__ void __launch_bounds__(kB2Threads, 4)
         z.ubp = q3.x;
       }
       const float tau = fminf(z.ubp, tcf);
-      const unsigned fl0 = __float_as_uint(ws.zref[13]);
+      const unsigned fl0 = __float_as_uint(q3.y);
+      const float zZ2 = q3.z, zKz = q3.w;
       bool ka, kb;
       if constexpr (KIND == kVoronoi && BM) {
       // Voronoi brick lists: a second reference, the next-least upper bound
@@ -742,6 +898,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
         zr[6] = o.mx[0], zr[7] = o.mx[1], zr[8] = o.mx[2];
         zr[9] = o.t, zr[10] = o.lb, zr[11] = o.ub, zr[12] = o.ubp;
         zr[13] = __uint_as_float(rhi1 ? flb : fla);
+        ref_consts(o, Bs, e_d, zr[14], zr[15]);
       }
       __syncwarp();
       auto keep2 = [&](const SiteF& sx, unsigned flx, int slot) {
@@ -754,19 +911,20 @@ __global__ void __launch_bounds__(kB2Threads, 4)
         z2.mn[0] = q0.w, z2.mn[1] = q1.x, z2.mn[2] = q1.y;
         z2.mx[0] = q1.z, z2.mx[1] = q1.w, z2.mx[2] = q2.x;
         z2.t = q2.y, z2.lb = q2.z, z2.ub = q2.w;
-        return bisector_keep<KIND, PER>(sx, flx, z2, __float_as_uint(ws.zref2[13]), Bs, halfLf, invG, e_d);
+        const float4 q3b = *reinterpret_cast<const float4*>(&ws.zref2[12]);
+        return bisector_keep<KIND, PER>(sx, flx, z2, __float_as_uint(q3b.y), Bs, halfLf, invG, e_d, q3b.z, q3b.w);
       };
       ka = va && (lane == r0 || (sa.lbp <= tau &&
-                                            bisector_keep<KIND, PER>(sa, fla, z, fl0, Bs, halfLf, invG, e_d) &&
+                                            bisector_keep<KIND, PER>(sa, fla, z, fl0, Bs, halfLf, invG, e_d, zZ2, zKz) &&
                                             keep2(sa, fla, lane)));
       kb = vb && (lane + 32 == r0 || (sb.lbp <= tau &&
-                                                 bisector_keep<KIND, PER>(sb, flb, z, fl0, Bs, halfLf, invG, e_d) &&
+                                                 bisector_keep<KIND, PER>(sb, flb, z, fl0, Bs, halfLf, invG, e_d, zZ2, zKz) &&
                                                  keep2(sb, flb, lane + 32)));
       } else {
       ka = va && (lane == r0 || (sa.lbp <= tau &&
-                                            bisector_keep<KIND, PER>(sa, fla, z, fl0, Bs, halfLf, invG, e_d)));
+                                            bisector_keep<KIND, PER>(sa, fla, z, fl0, Bs, halfLf, invG, e_d, zZ2, zKz)));
       kb = vb && (lane + 32 == r0 || (sb.lbp <= tau &&
-                                                 bisector_keep<KIND, PER>(sb, flb, z, fl0, Bs, halfLf, invG, e_d)));
+                                                 bisector_keep<KIND, PER>(sb, flb, z, fl0, Bs, halfLf, invG, e_d, zZ2, zKz)));
       }
       // survivors -> the sub-brick's kSlot fixed slots (or the overflow
       // list when longer), in slot (= site index) order
@@ -1075,6 +1233,10 @@ struct __align__(16) Eval16Smem {
   int cnt[kFcap];
 };
 
+#ifndef VX_E16_UNROLL
+#define VX_E16_UNROLL 1
+#endif
+constexpr int kE16Unroll = VX_E16_UNROLL;
 template <int KIND, bool PER, bool FA>
 __global__ void __launch_bounds__(32, VX_EVAL16_MINB)
     eval16_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, const int2* __restrict__ info,
@@ -1143,6 +1305,7 @@ __global__ void __launch_bounds__(32, VX_EVAL16_MINB)
     bj[k] = 0;
   }
   const bool g1 = g.g_is_one;
+#pragma unroll kE16Unroll
   for (int j = 0; j < n2; ++j) {
     const double wz0 = ws.T[j][16 + vz], wz1 = ws.T[j][20 + vz];
     const double wy0 = ws.T[j][8 + vy], wy1 = ws.T[j][12 + vy];
