@@ -15,12 +15,13 @@
 //            (f32 coordinates relative to the super-brick centre, time, binned
 //            position, periodic-ambiguity flags); sites that cannot reach any
 //            voxel within the cutoff are dropped; the kept sites are
-//            rank-sorted by site index once.
+//            rank-sorted by site index once (a carry-chain count) and moved
+//            into index order.
 //   column : each warp owns a column of nbb 8^3 bricks: one pass computes every
 //            site's upper bound of prox for all bricks of the column (the x/y
 //            terms are shared) -> per-brick tau; a second pass the lower bounds
-//            -> a per-site keep mask; each brick's list is a ballot over its
-//            mask bit, in site-index order.
+//            -> a per-site keep mask; the column's brick lists are ballots
+//            over the mask bits, all built in one pass, in site-index order.
 //   sub-brick : per 8 x 8 x 4 sub-brick, tau + bisector cull against the site
 //            with the least upper bound -> the survivors' binned positions, in
 //            site order, into 16 fixed slots (longer lists: an overflow list),
@@ -65,14 +66,6 @@ constexpr int kLcapD = 128;
 constexpr int kSlot = 16;         // fixed list slots per sub-brick (longer lists: overflow list)
 constexpr int kRows2 = 256;       // cell rows per super-brick
 constexpr float kRel = 1e-5f;
-#ifndef VX_COL_OLD
-#define VX_COL_OLD 0
-#endif
-// the gathered sites are moved into site-index order after the rank sort
-// (instead of an index permutation read by every brick's list pass)
-#ifndef VX_PERMUTE
-#define VX_PERMUTE 1
-#endif
 
 struct FBox {
   float c[3];  // centre relative to the super-brick centre
@@ -84,6 +77,7 @@ struct __align__(16) WarpSmem {
   int L[kLcapD];       // dense mode: a sub-brick's survivors (binned positions)
   float4 bxy;          // the column's x/y box (c[0], c[1], h[0], h[1]), shared by its sub-bricks
   unsigned evals;      // exact evaluations the eval kernel will do for this warp's sub-bricks
+  int nw[4];           // standard lists: the column's brick-list lengths
   alignas(16) float zref2[16]; // the second reference (VX_TWO_REFS)
   alignas(16) float zref[16];  // the sub-brick's reference site: SiteF fields + flags (written by its lane)
 };
@@ -105,7 +99,6 @@ struct Smem2 {
   int p[kTcap];        // binned position
   int idx[kTcap];      // original site index
   unsigned char flag[kTcap];  // bit a: periodic image ambiguous on axis a
-  short ord[kTcap];    // gather slots in ascending site-index order
   unsigned char mk[kB2Threads / 32][kTcap];  // per warp: bit b = kept for brick b of its column
   int seg_start[2 * kRows2];
   int seg_off[2 * kRows2 + 1];
@@ -115,7 +108,7 @@ struct Smem2 {
   double cx[kSB], cy[kSB], cz[kSZ];  // exact voxel centres of the super-brick
   union {
     WarpSmem w[kB2Threads / 32];
-    struct {  // VX_PERMUTE: the gather's staging arrays (dead once the sites are in order)
+    struct {  // the gather's staging arrays (dead once the sites are in index order)
       float4 rel[kTcap];
       int p[kTcap];
       unsigned char flag[kTcap];
@@ -465,15 +458,9 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       base = __shfl_sync(0xffffffffu, base, 0);
       const int pos = base + __popc(m & ((1u << lane) - 1u));
       if (keep && pos < kTcap) {
-#if VX_PERMUTE
         S.g.rel[pos] = make_float4(uf[0], uf[1], uf[2], (float)tv);
         S.g.p[pos] = p;
         S.g.flag[pos] = (unsigned char)fl;
-#else
-        S.rel[pos] = make_float4(uf[0], uf[1], uf[2], (float)tv);
-        S.p[pos] = p;
-        S.flag[pos] = (unsigned char)fl;
-#endif
         S.idx[pos] = bins.idx[p];
       }
     }
@@ -501,13 +488,10 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       }
       const unsigned rank = 4u * (unsigned)nk - ge;
       VXCHK(rank < (unsigned)T);
-#if VX_PERMUTE
+      // the kept sites move into site-index order
       S.rel[rank] = S.g.rel[f];
       S.p[rank] = S.g.p[f];
       S.flag[rank] = S.g.flag[f];
-#else
-      S.ord[rank] = (short)f;
-#endif
     }
   }
   __syncthreads();
@@ -582,7 +566,6 @@ __global__ void __launch_bounds__(kB2Threads, 4)
   };
   if (!col_any) return;  // no barrier follows
   if (cta_ok) {
-#if !VX_COL_OLD
     // Column passes.  A periodic-ambiguous axis (flag bit a) is fed in as a
     // NaN coordinate: fminf(NaN, L/2) = L/2 (the upper bound's cap) and
     // fmaxf(NaN, 0) = 0 (the lower bound's), so no per-brick flag test.  For
@@ -660,63 +643,29 @@ __global__ void __launch_bounds__(kB2Threads, 4)
     };
     if (nbb == kMaxBB) pass2(std::integral_constant<int, kMaxBB>{});
     else pass2(std::integral_constant<int, 0>{});
-#else
-    float myub[kMaxBB];
-#pragma unroll
-    for (int b = 0; b < kMaxBB; ++b) myub[b] = __int_as_float(0x7f800000);
-    for (int f = lane; f < T; f += 32) {
-      const float4 s = S.rel[f];
-      const unsigned fl = S.flag[f];
-      float mx = fabsf(s.x - Bxy.c[0]) + Bxy.h[0];
-      float my = fabsf(s.y - Bxy.c[1]) + Bxy.h[1];
-      if (PER) {
-        mx = (fl & 1u) ? halfLf[0] : fminf(mx, halfLf[0]);
-        my = (fl & 2u) ? halfLf[1] : fminf(my, halfLf[1]);
-      }
-      const float bxy = __fmaf_rn(my, my, mx * mx);
+    __syncwarp();
+  }
+  // standard lists: every brick's list of the column in one pass over the
+  // gathered sites (brick b in W[64 b, 64 b + 64)), in site-index order
+  if (!DENSE && lists_ok) {
+    int nWb[kMaxBB] = {0, 0, 0, 0};
+    const unsigned lt = (1u << lane) - 1u;
+    for (int f0 = 0; f0 < T; f0 += 32) {
+      const int f = f0 + lane;
+      const unsigned m = f < T ? S.mk[wid][f] : 0u;
 #pragma unroll
       for (int b = 0; b < kMaxBB; ++b) {
-        if (b >= nbb) break;
-        float mz = fabsf(s.z - bzc[b]) + bzh[b];
-        if (PER) mz = (fl & 4u) ? halfLf[2] : fminf(mz, halfLf[2]);
-        const float ub = __fmaf_rn(mz, mz, bxy) * (1.f + kRel);
-        myub[b] = fminf(myub[b], KIND == kVoronoi ? ub
-                                                  : hi_add((KIND == kJohnsonMehl ? sqrtf(ub) : ub) * invG * (1.f + kRel),
-                                                           s.w + kRel * fabsf(s.w)));
+        const bool keep = (m >> b) & 1u;
+        const unsigned bm = __ballot_sync(0xffffffffu, keep);
+        const int pos = nWb[b] + __popc(bm & lt);
+        if (keep && pos < kWcap) ws.W[b * kWcap + pos] = f;
+        nWb[b] += __popc(bm);
       }
     }
+    if (lane == 0) {
 #pragma unroll
-    for (int b = 0; b < kMaxBB; ++b) {
-      float t = myub[b];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) t = fminf(t, __shfl_xor_sync(0xffffffffu, t, o));
-      tau[b] = fminf(t, tcf);
+      for (int b = 0; b < kMaxBB; ++b) ws.nw[b] = nWb[b];
     }
-    for (int f = lane; f < T; f += 32) {
-      const float4 s = S.rel[f];
-      const unsigned fl = S.flag[f];
-      float lx = fmaxf(fabsf(s.x - Bxy.c[0]) - Bxy.h[0], 0.f);
-      float ly = fmaxf(fabsf(s.y - Bxy.c[1]) - Bxy.h[1], 0.f);
-      if (PER) {
-        if (fl & 1u) lx = 0.f;
-        if (fl & 2u) ly = 0.f;
-      }
-      const float bxy = __fmaf_rn(ly, ly, lx * lx);
-      unsigned m = 0;
-#pragma unroll
-      for (int b = 0; b < kMaxBB; ++b) {
-        if (b >= nbb) break;
-        float lz = fmaxf(fabsf(s.z - bzc[b]) - bzh[b], 0.f);
-        if (PER && (fl & 4u)) lz = 0.f;
-        const float lb = __fmaf_rn(lz, lz, bxy) * (1.f - kRel);
-        const float lbp = KIND == kVoronoi ? lb
-                                           : lo_add((KIND == kJohnsonMehl ? sqrtf(lb) : lb) * invG * (1.f - kRel),
-                                                    s.w - kRel * fabsf(s.w));
-        if (bval[b] && lbp <= tau[b]) m |= 1u << b;
-      }
-      S.mk[wid][f] = (unsigned char)m;
-    }
-#endif
     __syncwarp();
   }
 
@@ -727,9 +676,19 @@ __global__ void __launch_bounds__(kB2Threads, 4)
 
   int nW = 0;
   bool brick_ok = lists_ok;
-  if (brick_ok) {
+  const int* Wl = ws.W;  // this brick's list
+  if (!DENSE) {
+    nW = lists_ok ? ws.nw[bb] : 0;
+    Wl = ws.W + bb * kWcap;
+    brick_ok = lists_ok && nW <= kWcap;
+    if (VX_STATS_ON && lane == 0 && lists_ok) {
+      atomicAdd(&eval_slots[67], (unsigned long long)nW);
+      atomicAdd(&eval_slots[68], 1ull);
+      atomicMax(&eval_slots[72], (unsigned long long)nW);
+    }
+  } else if (brick_ok) {
     for (int f0 = 0; f0 < T; f0 += 32) {
-      const int f = f0 + lane < T ? (VX_PERMUTE ? f0 + lane : S.ord[f0 + lane]) : 0;
+      const int f = f0 + lane < T ? f0 + lane : 0;
       const bool keep = f0 + lane < T && ((S.mk[wid][f] >> bb) & 1u);
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       const int pos = nW + __popc(m & ((1u << lane) - 1u));
@@ -835,7 +794,7 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       // one bound evaluation per brick-list site, kept in registers (slots
       // lane and lane + 32; nW <= 64)
       const bool va = lane < nW, vb = lane + 32 < nW;
-      const int fa = va ? ws.W[lane] : 0, fb = vb ? ws.W[lane + 32] : 0;
+      const int fa = va ? Wl[lane] : 0, fb = vb ? Wl[lane + 32] : 0;
       const unsigned fla = va ? S.flag[fa] : 0u, flb = vb ? S.flag[fb] : 0u;
       SiteF sa, sb;
       fbounds<KIND, PER>(S.rel[fa], fla, Bs, halfLf, invG, sa);
