@@ -529,7 +529,9 @@ __global__ void __launch_bounds__(kB2Threads, 4)
   const int ex0 = min(8, ext[0] - bxo), ex1 = min(8, ext[1] - byo);
   float bzc[kMaxBB], bzh[kMaxBB], tau[kMaxBB];
   bool bval[kMaxBB];
-  FBox Bxy;
+  // the column's x/y extent once (an empty column, ex0 or ex1 <= 0, returns
+  // below: the indices stay inside cx / cy), each brick's z extent
+  const FBox Bxy = box_of(bxo, byo, 0, max(ex0, 1), max(ex1, 1), 1);
 #pragma unroll
   for (int b = 0; b < kMaxBB; ++b) {
     const int bzo = (wid >> 2) * 8 + 16 * b;
@@ -539,10 +541,9 @@ __global__ void __launch_bounds__(kB2Threads, 4)
     bzh[b] = 0.f;
     tau[b] = -1.f;
     if (bval[b]) {
-      const FBox B = box_of(bxo, byo, bzo, ex0, ex1, ez);
-      Bxy = B;
-      bzc[b] = B.c[2];
-      bzh[b] = B.h[2];
+      const double l = S.cz[bzo], h = S.cz[bzo + ez - 1];
+      bzc[b] = (float)(0.5 * (l + h) - cc[2]);
+      bzh[b] = (float)(0.5 * (h - l)) * (1.f + kRel) + 2.f * e_d;
     }
   }
   bool col_any = false;
@@ -1054,8 +1055,20 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 32 / kEvalWarps)
         }
       }
     };
-    if (vmask == 0xFFu) resolve(std::true_type{});
-    else resolve(std::false_type{});
+    bool allin = true;  // every voxel of the lane within the cutoff
+#pragma unroll
+    for (int k = 0; k < 8; ++k) allin &= best[k] <= cutoff;
+    if (__all_sync(0xffffffffu, vmask == 0xFFu && allin)) {  // the common case: straight-line
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        lab[k] = ws.Fidx[bj[k]];
+        if (hist) atomicAdd(&ws.cnt[bj[k]], 1);
+      }
+    } else if (vmask == 0xFFu) {
+      resolve(std::true_type{});
+    } else {
+      resolve(std::false_type{});
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (!((vmask >> (4 * h)) & 0xFu)) continue;
@@ -1316,8 +1329,22 @@ __global__ void __launch_bounds__(32, VX_EVAL16_MINB)
       }
     }
   };
-  if (vmask == 0xFFFFu) resolve(std::true_type{});
-  else resolve(std::false_type{});
+  bool allin = true;  // every voxel of the lane within the cutoff
+#pragma unroll
+  for (int k = 0; k < 16; ++k) allin &= best[k] <= cutoff;
+  if (__all_sync(0xffffffffu, vmask == 0xFFFFu && allin)) {
+    // the common case (whole brick inside the grid and inside the balls):
+    // straight-line label lookups and histogram counts
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      lab[k] = ws.Fidx[bj[k]];
+      if (hist) atomicAdd(&ws.cnt[bj[k]], 1);
+    }
+  } else if (vmask == 0xFFFFu) {
+    resolve(std::true_type{});
+  } else {
+    resolve(std::false_type{});
+  }
   const long long slab_z = (long long)bz * 8 + vz;  // z inside the slab
   // row r = 2 zh + yh: voxel offset of its first x, rows 4 planes / 4 rows apart
   const long long vox0 = slab_z * g.plane + (long long)(y0 + vy) * g.n[0] + x0 + qx;
