@@ -24,15 +24,16 @@ for cfg in [int(x) for x in sys.argv[1:]] or [2, 3, 4, 5]:
     hist = torch.zeros(p.n_sites, dtype=torch.int64, device="cuda")
     kw = dict(kind=p.kind, counts=list(p.counts), lengths=list(p.lengths), periodic=p.periodic,
               positions=pos, times=t, growth=p.growth, labels=lab, histogram=hist)
-    balls, cull = [], []
+    balls, cull, shells = [], [], []
     for i in range(reps + 2):
         st = eng.run(profile=True, **kw)
         if i >= 2:
             balls.append(st["stage_ms"]["ball"])
+            shells.append(st["stage_ms"]["shell"])
     fp = oracle.fingerprint(lab.cpu().numpy())
     ok = fp == oracle.SURVEY_FINGERPRINTS[cfg]
     print(f"{os.path.basename(tag):28s} cfg{cfg} ball median {np.median(balls):.3f} min {np.min(balls):.3f} ms "
-          f"{'OK' if ok else 'FAIL ' + fp}", flush=True)
+          f"{'OK' if ok else 'FAIL ' + fp} shell {np.median(shells):.3f}", flush=True)
     eng.close()
     del lab, hist, pos
     torch.cuda.empty_cache()
