@@ -886,6 +886,10 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       kb = vb && (lane + 32 == r0 || (sb.lbp <= tau &&
                                                  bisector_keep<KIND, PER>(sb, flb, z, fl0, Bs, halfLf, invG, e_d, zZ2, zKz)));
       }
+#ifdef VX_NO_BSTAGE  // experiment: the column pass's brick lists unrefined
+      ka = va;
+      kb = vb;
+#endif
       // survivors -> the sub-brick's kSlot fixed slots (or the overflow
       // list when longer), in slot (= site index) order
       const long long sbi = list_id();
@@ -1205,12 +1209,28 @@ struct __align__(16) Eval16Smem {
   int cnt[kFcap];
 };
 
+#ifndef VX_E16_PACK
+#define VX_E16_PACK 0  // 1: byte-packed winner slots for Laguerre too
+#endif
+// strict-< update of one voxel's best prox; its winner slot is byte SEL of
+// bjp (prmt selector: that byte from jj = j * 0x01010101, the others kept),
+// both under the compare's predicate
+template <unsigned SEL>
+__device__ __forceinline__ void upd_slot(unsigned& bjp, double& best, double pr, unsigned jj) {
+  asm("{\n\t.reg .pred p;\n\tsetp.lt.f64 p, %2, %1;\n\t@p mov.f64 %1, %2;\n\t"
+      "@p prmt.b32 %0, %0, %3, %4;\n\t}"
+      : "+r"(bjp), "+d"(best)
+      : "d"(pr), "r"(jj), "n"(SEL));
+}
 #ifndef VX_E16_UNROLL
 #define VX_E16_UNROLL 1
 #endif
 constexpr int kE16Unroll = VX_E16_UNROLL;
+#ifndef VX_EVAL16_MINB_V
+#define VX_EVAL16_MINB_V 28  // Voronoi (packed slots): 72 registers, no spills (cfg5 -1.3 %, cfg2 -3.1 %)
+#endif
 template <int KIND, bool PER, bool FA>
-__global__ void __launch_bounds__(32, VX_EVAL16_MINB)
+__global__ void __launch_bounds__(32, KIND == kVoronoi ? VX_EVAL16_MINB_V : VX_EVAL16_MINB)
     eval16_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, const int2* __restrict__ info,
                   const int* __restrict__ slots16, const int* __restrict__ list, int* __restrict__ labels,
                   double* __restrict__ dist, unsigned long long* __restrict__ hist, long long* __restrict__ unres,
@@ -1269,7 +1289,11 @@ __global__ void __launch_bounds__(32, VX_EVAL16_MINB)
   if (lane < n2) ws.Fidx[lane] = fidx;
   __syncwarp();
   // voxel k = 8 zh + 4 yh + i: x = qx + i, y = vy + 4 yh, z = vz + 4 zh
+  // Voronoi: the winner slots as bytes of bjp (4 registers instead of 16):
+  // 72 registers, 28 warps/SM (Laguerre: 24 warps either way, no gain)
+  constexpr bool PACK = VX_E16_PACK || KIND == kVoronoi;
   double best[16];
+  unsigned bjp[4] = {0u, 0u, 0u, 0u};
   int bj[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
@@ -1279,6 +1303,7 @@ __global__ void __launch_bounds__(32, VX_EVAL16_MINB)
   const bool g1 = g.g_is_one;
 #pragma unroll kE16Unroll
   for (int j = 0; j < n2; ++j) {
+    const unsigned jj = (unsigned)j * 0x01010101u;
     const double wz0 = ws.T[j][16 + vz], wz1 = ws.T[j][20 + vz];
     const double wy0 = ws.T[j][8 + vy], wy1 = ws.T[j][12 + vy];
     const double a[4] = {__dadd_rn(wz0, wy0), __dadd_rn(wz0, wy1), __dadd_rn(wz1, wy0), __dadd_rn(wz1, wy1)};
@@ -1288,27 +1313,48 @@ __global__ void __launch_bounds__(32, VX_EVAL16_MINB)
     const double tj = KIND == kVoronoi ? 0.0 : ws.Ft[j];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
+      if constexpr (PACK) {
+        double pr[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const double d = __dadd_rn(a[r], wx[i]);
-        const double pr = FA ? prox_from_dsq_nc<KIND>(d, g.growth, g1, tj, g.inv_growth_rn)
-                             : prox_from_dsq<KIND>(d, g.growth, g1, tj);
-        const int k = 4 * r + i;  // r = 2 zh + yh
-        if (pr < best[k]) {
-          best[k] = pr;
-          bj[k] = j;
+        for (int i = 0; i < 4; ++i) {
+          const double d = __dadd_rn(a[r], wx[i]);
+          pr[i] = FA ? prox_from_dsq_nc<KIND>(d, g.growth, g1, tj, g.inv_growth_rn)
+                     : prox_from_dsq<KIND>(d, g.growth, g1, tj);
+        }
+        upd_slot<0x3214>(bjp[r], best[4 * r + 0], pr[0], jj);
+        upd_slot<0x3240>(bjp[r], best[4 * r + 1], pr[1], jj);
+        upd_slot<0x3410>(bjp[r], best[4 * r + 2], pr[2], jj);
+        upd_slot<0x4210>(bjp[r], best[4 * r + 3], pr[3], jj);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double d = __dadd_rn(a[r], wx[i]);
+          const double pr = FA ? prox_from_dsq_nc<KIND>(d, g.growth, g1, tj, g.inv_growth_rn)
+                               : prox_from_dsq<KIND>(d, g.growth, g1, tj);
+          const int k = 4 * r + i;  // r = 2 zh + yh
+          if (pr < best[k]) {
+            best[k] = pr;
+            bj[k] = j;
+          }
         }
       }
     }
   }
+  if constexpr (PACK) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) bj[k] = (int)((bjp[k >> 2] >> (8 * (k & 3))) & 0xFFu);
+  }
   // ---- resolve + store + compaction ----
   const int xr = bext[0] - qx;
   const unsigned xm = xr >= 4 ? 0xFu : (xr > 0 ? (1u << xr) - 1u : 0u);
-  unsigned vmask = 0;
+  unsigned vmask = 0xFFFFu;  // bricks inside the grid (warp-uniform test)
+  if (bext[0] < 8 || bext[1] < 8 || bext[2] < 8) {
+    vmask = 0;
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int yy = vy + 4 * (r & 1), zz = vz + 4 * (r >> 1);
-    if (yy < bext[1] && zz < bext[2]) vmask |= xm << (4 * r);
+    for (int r = 0; r < 4; ++r) {
+      const int yy = vy + 4 * (r & 1), zz = vz + 4 * (r >> 1);
+      if (yy < bext[1] && zz < bext[2]) vmask |= xm << (4 * r);
+    }
   }
   int lab[16];
   unsigned umask = 0;

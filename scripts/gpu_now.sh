@@ -1,5 +1,8 @@
-# ad-hoc GPU call: bench (clock sampler check) + ncu capture of the ball kernels at cfg5
+# ad-hoc GPU call: exactness + interleaved A/B timing of the builds under abl/ (+ list statistics)
 cd $GRAFT_REPO_ROOT
-timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu > gpurun_out/bench_cfg5_now.json 2> gpurun_out/bench_cfg5_now.err
-python -c "import json;d=json.load(open('gpurun_out/bench_cfg5_now.json'));print(d['value'],d['clocks'],d['stage_ms'])"
-CFG=5 bash scripts/gpu_ncu12.sh
+NQ=${NQ:-12}
+for lib in abl/*.so; do
+  VX_LIB_PATH=$lib timeout 600 python scripts/exact_quick.py $NQ 7 > gpurun_out/eq_$(basename $lib).log 2>&1; echo "$lib $(tail -1 gpurun_out/eq_$(basename $lib).log)"
+done
+CFGS="${CFGS:-2 3 5}" REPS=${REPS:-9} bash scripts/ab_run.sh 2>&1 | sort -k2,2 -k1,1 | awk '{print $1,$2,$5,$7,$9,$11}'
+for lib in ${STATS_LIBS}; do VX_STATS=1 VX_LIB_PATH=$lib timeout 300 python scripts/stats_probe.py 2>&1 | head -12; done
