@@ -568,8 +568,9 @@ __global__ void __launch_bounds__(kB2Threads, 4)
   if (!col_any) return;  // no barrier follows
   if (cta_ok) {
     // Column passes.  A periodic-ambiguous axis (flag bit a) is fed in as a
-    // NaN coordinate: fminf(NaN, L/2) = L/2 (the upper bound's cap) and
-    // fmaxf(NaN, 0) = 0 (the lower bound's), so no per-brick flag test.  For
+    // NaN coordinate: the site drops out of the upper bounds' minimum and
+    // fmaxf(NaN, 0) = 0 makes the lower bound's axis term 0, so no per-brick
+    // flag test.  For
     // Voronoi the (1 + kRel) widening commutes with the minimum (RN(x c) is
     // monotone in x) and the lower-bound test lb (1 - kRel) <= tau is replaced
     // by the weaker lb <= tau / (1 - kRel) (1 + 1e-6): a superset is kept.
@@ -586,18 +587,17 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       const float sx = PER && (fl & 1u) ? qnan : s.x;
       const float sy = PER && (fl & 2u) ? qnan : s.y;
       const float sz = PER && (fl & 4u) ? qnan : s.z;
-      float mx = fabsf(sx - Bxy.c[0]) + Bxy.h[0];
-      float my = fabsf(sy - Bxy.c[1]) + Bxy.h[1];
-      if (PER) {
-        mx = fminf(mx, halfLf[0]);
-        my = fminf(my, halfLf[1]);
-      }
+      // no L/2 cap: on an unflagged axis |s - c| + h < L/2 already (up to the
+      // widening, which only raises the bound), and a flagged (NaN) axis makes
+      // the bound NaN, which fminf ignores -- a site left out of the minimum
+      // only raises tau, so the cull stays conservative
+      const float mx = fabsf(sx - Bxy.c[0]) + Bxy.h[0];
+      const float my = fabsf(sy - Bxy.c[1]) + Bxy.h[1];
       const float bxy = __fmaf_rn(my, my, mx * mx);
 #pragma unroll
       for (int b = 0; b < kMaxBB; ++b) {
         if (NB == 0 && b >= nbb) break;
-        float mz = fabsf(sz - bzc[b]) + bzh[b];
-        if (PER) mz = fminf(mz, halfLf[2]);
+        const float mz = fabsf(sz - bzc[b]) + bzh[b];
         const float u2 = __fmaf_rn(mz, mz, bxy);
         myub[b] = fminf(myub[b], KIND == kVoronoi ? u2
                                                   : hi_add((KIND == kJohnsonMehl ? sqrtf(u2 * (1.f + kRel)) : u2 * (1.f + kRel)) * invG * (1.f + kRel),
