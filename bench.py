@@ -527,7 +527,7 @@ def run_ours(args):
     peak = dadd.value / 1e12
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None, "traffic": load_traffic(args.config),
-                "kernel": "ball phase (cull12_kernel + " + ("eval12_kernel" if c["kind"] == 1 else "eval16_kernel") + ")",
+                "kernel": "ball phase (cull12_kernel + eval16_kernel)",
                 "kernel_ms": ball_ms,
                 "algorithmic": f"{c_kind:g} f64 ops x N_v(ln N_s + 1) = {evals * c_kind:.4g} per launch",
                 "peak_source": "measured DADD issue rate (vx_probe_pipe_rates) on this GPU",

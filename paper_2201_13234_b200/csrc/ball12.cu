@@ -1209,6 +1209,9 @@ struct __align__(16) Eval16Smem {
   int cnt[kFcap];
 };
 
+#ifndef VX_JM_BRICKS
+#define VX_JM_BRICKS 1
+#endif
 #ifndef VX_E16_PACK
 #define VX_E16_PACK 0  // 1: byte-packed winner slots for Laguerre too
 #endif
@@ -1289,9 +1292,10 @@ __global__ void __launch_bounds__(32, KIND == kVoronoi ? VX_EVAL16_MINB_V : VX_E
   if (lane < n2) ws.Fidx[lane] = fidx;
   __syncwarp();
   // voxel k = 8 zh + 4 yh + i: x = qx + i, y = vy + 4 yh, z = vz + 4 zh
-  // Voronoi: the winner slots as bytes of bjp (4 registers instead of 16):
-  // 72 registers, 28 warps/SM (Laguerre: 24 warps either way, no gain)
-  constexpr bool PACK = VX_E16_PACK || KIND == kVoronoi;
+  // Voronoi / JM: the winner slots as bytes of bjp (4 registers instead of
+  // 16): Voronoi 72 registers, 28 warps/SM; JM fits 80 without spills
+  // (Laguerre: 24 warps either way, no gain)
+  constexpr bool PACK = VX_E16_PACK || KIND == kVoronoi || KIND == kJohnsonMehl;
   double best[16];
   unsigned bjp[4] = {0u, 0u, 0u, 0u};
   int bj[16];
@@ -1520,10 +1524,11 @@ static int launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* l
   const bool attr = (attr_done.load() & bit) != 0;
   const size_t sh_c = sizeof(v12::Smem2);
   const size_t sh_e = sizeof(v12::EvalSmemT<DENSE ? v12::kLcapD : v12::kFcap>) * v12::kEvalWarps;
-  // brick lists + eval16 for Voronoi and Laguerre (JM keeps sub-brick lists:
-  // its in-loop sqrt needs the registers eval16 spends on 16 voxels per lane)
+  // brick lists + eval16 for every kind (JM: with the packed winner slots its
+  // in-loop sqrt fits eval16's 80 registers, cfg4 -1.2 %); dense mode and
+  // VX_SUBBRICK_LISTS=1 use sub-brick lists + eval12
   static const bool sub_env = std::getenv("VX_SUBBRICK_LISTS") != nullptr;
-  const bool bl = !DENSE && KIND != kJohnsonMehl && !sub_env;
+  const bool bl = !DENSE && (KIND != kJohnsonMehl || VX_JM_BRICKS) && !sub_env;
   if (!attr) {
     cudaFuncSetAttribute(v12::cull12_kernel<KIND, PER, DENSE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sh_c);
@@ -1550,7 +1555,7 @@ static int launch12(const Geo& g, const Bins& bins, const DevParams* prm, int* l
           g, bins, prm, info, slots16, list, list_cap, list_count, ovf, ctr, slots, nbb, (unsigned)y0);
   }
   const long long nsb = ball12_subbricks(g);
-  if constexpr (KIND != kJohnsonMehl) if (bl) {
+  if constexpr (KIND != kJohnsonMehl || VX_JM_BRICKS) if (bl) {
     const size_t sh16 = sizeof(v12::Eval16Smem);
     if (!attr) {
       cudaFuncSetAttribute(v12::eval16_kernel<KIND, PER, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh16);

@@ -398,9 +398,12 @@ def test_baseline_config_fingerprints(oracle_mod, k):
         del ref, hist
 
 
-@pytest.mark.parametrize("ver", [12])
-def test_every_ball_kernel_variant(ver):
-    """Each ball-kernel generation stays bit-exact (selected with VX_BALL)."""
+@pytest.mark.parametrize("route", ["bricks", "subbricks", "dense"])
+def test_every_ball_kernel_variant(route):
+    """Each ball-phase route stays bit-exact: the default brick lists + eval16,
+    the 8 x 8 x 4 sub-brick lists + eval12 (VX_SUBBRICK_LISTS=1) and dense
+    mode (VX_DENSE=1) -- random 2-D / 3-D instances of every kind against the
+    oracle, the cfg1 and cfg4 (Johnson-Mehl) fingerprints."""
     code = r"""
 import sys, numpy as np
 sys.path.insert(0, %r); sys.path.insert(0, %r)
@@ -420,13 +423,20 @@ for i in range(36):
     lab, dist = oracle.brute(p)
     assert np.array_equal(r.labels.labels, lab), i
     assert np.array_equal(r.distances.values.view(np.uint64), dist.view(np.uint64)), i
-cfg = oracle.baseline_config(1)
-s, g = to_vx(cfg)
-r = vx.tessellate_fast(s, g, distances=False)
-assert oracle.fingerprint(r.labels.labels) == oracle.SURVEY_FINGERPRINTS[1]
+for k in (1, 4):
+    cfg = oracle.baseline_config(k)
+    s, g = to_vx(cfg)
+    r = vx.tessellate_fast(s, g, distances=False)
+    assert oracle.fingerprint(r.labels.labels) == oracle.SURVEY_FINGERPRINTS[k], k
 print("ok")
 """ % (ROOT, os.path.join(ROOT, "tests"))
-    env = dict(os.environ, VX_BALL=str(ver))
+    env = dict(os.environ)
+    env.pop("VX_SUBBRICK_LISTS", None)
+    env.pop("VX_DENSE", None)
+    if route == "subbricks":
+        env["VX_SUBBRICK_LISTS"] = "1"
+    elif route == "dense":
+        env["VX_DENSE"] = "1"
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
