@@ -1213,7 +1213,7 @@ struct __align__(16) Eval16Smem {
 #define VX_JM_BRICKS 1
 #endif
 #ifndef VX_E16_PACK
-#define VX_E16_PACK 0  // 1: byte-packed winner slots for Laguerre too
+#define VX_E16_PACK 1  // 0: one slot register per voxel (A/B)
 #endif
 // strict-< update of one voxel's best prox; its winner slot is byte SEL of
 // bjp (prmt selector: that byte from jj = j * 0x01010101, the others kept),
@@ -1230,10 +1230,12 @@ __device__ __forceinline__ void upd_slot(unsigned& bjp, double& best, double pr,
 #endif
 constexpr int kE16Unroll = VX_E16_UNROLL;
 #ifndef VX_EVAL16_MINB_V
-#define VX_EVAL16_MINB_V 28  // Voronoi (packed slots): 72 registers, no spills (cfg5 -1.3 %, cfg2 -3.1 %)
+// Voronoi / Laguerre (packed slots): 72 registers (Voronoi no spills: cfg5
+// -1.3 %, cfg2 -3.1 %; Laguerre 4 B of spills: cfg3 -2.6 %); JM keeps 80
+#define VX_EVAL16_MINB_V 28
 #endif
 template <int KIND, bool PER, bool FA>
-__global__ void __launch_bounds__(32, KIND == kVoronoi ? VX_EVAL16_MINB_V : VX_EVAL16_MINB)
+__global__ void __launch_bounds__(32, KIND == kJohnsonMehl ? VX_EVAL16_MINB : VX_EVAL16_MINB_V)
     eval16_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, const int2* __restrict__ info,
                   const int* __restrict__ slots16, const int* __restrict__ list, int* __restrict__ labels,
                   double* __restrict__ dist, unsigned long long* __restrict__ hist, long long* __restrict__ unres,
@@ -1292,10 +1294,10 @@ __global__ void __launch_bounds__(32, KIND == kVoronoi ? VX_EVAL16_MINB_V : VX_E
   if (lane < n2) ws.Fidx[lane] = fidx;
   __syncwarp();
   // voxel k = 8 zh + 4 yh + i: x = qx + i, y = vy + 4 yh, z = vz + 4 zh
-  // Voronoi / JM: the winner slots as bytes of bjp (4 registers instead of
-  // 16): Voronoi 72 registers, 28 warps/SM; JM fits 80 without spills
-  // (Laguerre: 24 warps either way, no gain)
-  constexpr bool PACK = VX_E16_PACK || KIND == kVoronoi || KIND == kJohnsonMehl;
+  // the winner slots as bytes of bjp (4 registers instead of 16): Voronoi
+  // and Laguerre run at 72 registers / 28 warps per SM, JM's in-loop sqrt
+  // fits 80 without spills
+  constexpr bool PACK = VX_E16_PACK != 0;
   double best[16];
   unsigned bjp[4] = {0u, 0u, 0u, 0u};
   int bj[16];
