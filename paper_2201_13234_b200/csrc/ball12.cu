@@ -66,6 +66,9 @@ constexpr int kLcapD = 128;
 constexpr int kSlot = 16;         // fixed list slots per sub-brick (longer lists: overflow list)
 constexpr int kRows2 = 256;       // cell rows per super-brick
 constexpr float kRel = 1e-5f;
+#ifndef VX_COLSTAGE_V
+#define VX_COLSTAGE_V 0  // Voronoi keeps the per-brick loop (column stage: cfg5 +6.6 %, 44 B of spills)
+#endif
 
 struct FBox {
   float c[3];  // centre relative to the super-brick centre
@@ -74,12 +77,19 @@ struct FBox {
 
 struct __align__(16) WarpSmem {
   int W[kWcapD];       // brick list (gather slots), ascending site index
-  int L[kLcapD];       // dense mode: a sub-brick's survivors (binned positions)
+  union {
+    int L[kLcapD];     // dense mode: a sub-brick's survivors (binned positions)
+    struct {           // standard lists, column brick stage: per brick the two references
+      float zrefb[kMaxBB][16];
+      float zref2b[kMaxBB][16];
+    };
+  };
   float4 bxy;          // the column's x/y box (c[0], c[1], h[0], h[1]), shared by its sub-bricks
   unsigned evals;      // exact evaluations the eval kernel will do for this warp's sub-bricks
   int nw[4];           // standard lists: the column's brick-list lengths
   alignas(16) float zref2[16]; // the second reference (VX_TWO_REFS)
   alignas(16) float zref[16];  // the sub-brick's reference site: SiteF fields + flags (written by its lane)
+  float2 bzb[kMaxBB];   // each brick's z box (centre, half extent): box_sub's values
 };
 
 // eval12: per warp (one sub-brick); LC = list capacity
@@ -248,6 +258,28 @@ __device__ __forceinline__ bool bisector_keep(const SiteF& s, unsigned fs, const
   }
   q = q >= 0.f ? q * invG * (1.f - kRel) : q * invG * (1.f + kRel);
   return lo_add(q, dt) <= 0.f;
+}
+
+// a reference site's bounds through shared memory (16 floats: SiteF fields,
+// flags, ref_consts), written by its owner lane, read by every lane of its box
+__device__ __forceinline__ void put_ref(float* zr, const SiteF& o, unsigned fl, const FBox& B, float e_d) {
+  zr[0] = o.v[0], zr[1] = o.v[1], zr[2] = o.v[2];
+  zr[3] = o.mn[0], zr[4] = o.mn[1], zr[5] = o.mn[2];
+  zr[6] = o.mx[0], zr[7] = o.mx[1], zr[8] = o.mx[2];
+  zr[9] = o.t, zr[10] = o.lb, zr[11] = o.ub, zr[12] = o.ubp;
+  zr[13] = __uint_as_float(fl);
+  ref_consts(o, B, e_d, zr[14], zr[15]);
+}
+__device__ __forceinline__ void get_ref(const float* zr, SiteF& z, float4& q3) {
+  const float4 q0 = *reinterpret_cast<const float4*>(&zr[0]);
+  const float4 q1 = *reinterpret_cast<const float4*>(&zr[4]);
+  const float4 q2 = *reinterpret_cast<const float4*>(&zr[8]);
+  q3 = *reinterpret_cast<const float4*>(&zr[12]);
+  z.v[0] = q0.x, z.v[1] = q0.y, z.v[2] = q0.z;
+  z.mn[0] = q0.w, z.mn[1] = q1.x, z.mn[2] = q1.y;
+  z.mx[0] = q1.z, z.mx[1] = q1.w, z.mx[2] = q2.x;
+  z.t = q2.y, z.lb = q2.z, z.ub = q2.w;
+  z.ubp = q3.x;
 }
 
 __device__ __forceinline__ long long wrapi2(long long c, long long m) {
@@ -549,7 +581,13 @@ __global__ void __launch_bounds__(kB2Threads, 4)
   bool col_any = false;
 #pragma unroll
   for (int b = 0; b < kMaxBB; ++b) col_any |= bval[b];
-  if (lane == 0) ws.bxy = make_float4(Bxy.c[0], Bxy.c[1], Bxy.h[0], Bxy.h[1]);
+  if (lane == 0) {
+    ws.bxy = make_float4(Bxy.c[0], Bxy.c[1], Bxy.h[0], Bxy.h[1]);
+    if (BL && !DENSE && (KIND != kVoronoi || VX_COLSTAGE_V)) {  // the column brick stage's boxes
+#pragma unroll
+      for (int b = 0; b < kMaxBB; ++b) ws.bzb[b] = make_float2(bzc[b], bzh[b]);
+    }
+  }
   __syncwarp();
   // a sub-brick's box: the column's x/y extent (every sub-brick of the column
   // shares it) and its own z extent -- the values box_of would give
@@ -670,6 +708,191 @@ __global__ void __launch_bounds__(kB2Threads, 4)
     __syncwarp();
   }
 
+  // Column brick stage (brick lists): the refinement of every brick of the
+  // column in one pass -- brick b's list occupies slots [off_b, off_b + nW_b)
+  // of at most 64 (two per lane), arg-mins by warp reductions per brick,
+  // references through shared memory per brick.  Per site the same keep
+  // predicate, reference choice and slot order as the per-brick loop below
+  // (which handles columns whose lists total more than 64).
+  bool col_done = false;
+  if constexpr (BL && !DENSE && (KIND != kVoronoi || VX_COLSTAGE_V)) {
+    int nWe[kMaxBB];
+    bool bok[kMaxBB];
+#pragma unroll
+    for (int b = 0; b < kMaxBB; ++b) {
+      const int nwb = lists_ok && bval[b] ? ws.nw[b] : 0;
+      bok[b] = bval[b] && lists_ok && nwb <= kWcap;
+      nWe[b] = bok[b] ? nwb : 0;
+    }
+    const int o1 = nWe[0], o2 = o1 + nWe[1], o3 = o2 + nWe[2], M = o3 + nWe[3];
+    if (M <= 64) {
+      col_done = true;
+      auto okey = [](float v) -> unsigned {
+        const unsigned b = __float_as_uint(v);
+        return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+      };
+      auto bzo_of = [&](int b) { return (wid >> 2) * 8 + 16 * b; };
+      auto boxb = [&](int b) {  // == box_sub(bzo_of(b), min(8, ext[2] - bzo_of(b)))
+        FBox B;
+        const float4 xy = ws.bxy;
+        const float2 z = ws.bzb[b];
+        B.c[0] = xy.x, B.c[1] = xy.y, B.c[2] = z.x;
+        B.h[0] = xy.z, B.h[1] = xy.w, B.h[2] = z.y;
+        return B;
+      };
+      SiteF sv[2];
+      int fv[2], bv[2], kv[2];
+      unsigned flv[2];
+      bool vv[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int e = lane + 32 * i;
+        vv[i] = e < M;
+        const int b = (e >= o1) + (e >= o2) + (e >= o3);
+        bv[i] = b;
+        kv[i] = e - (b == 0 ? 0 : b == 1 ? o1 : b == 2 ? o2 : o3);
+        fv[i] = vv[i] ? ws.W[b * kWcap + kv[i]] : 0;
+        flv[i] = vv[i] ? S.flag[fv[i]] : 0u;
+        if (i == 1 && M <= 32) continue;
+        fbounds<KIND, PER>(S.rel[fv[i]], flv[i], boxb(b), halfLf, invG, sv[i]);
+      }
+      // per-brick packed (upper bound, slot) arg-min: one warp reduction per
+      // brick and iteration (REDUX), lanes of other bricks contribute ~0
+      auto brick_min = [&](const unsigned (&key)[2], unsigned (&res)[2]) {
+        unsigned km[kMaxBB];
+#pragma unroll
+        for (int b = 0; b < kMaxBB; ++b) {
+          km[b] = __reduce_min_sync(0xffffffffu, bv[0] == b ? key[0] : 0xffffffffu);
+          if (M > 32) km[b] = min(km[b], __reduce_min_sync(0xffffffffu, bv[1] == b ? key[1] : 0xffffffffu));
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) res[i] = bv[i] == 0 ? km[0] : bv[i] == 1 ? km[1] : bv[i] == 2 ? km[2] : km[3];
+      };
+      unsigned key[2], r0v[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) key[i] = vv[i] ? (okey(sv[i].ubp) & ~63u) | (unsigned)kv[i] : 0xffffffffu;
+      brick_min(key, r0v);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        r0v[i] &= 63u;
+        if (vv[i] && (unsigned)kv[i] == r0v[i]) put_ref(ws.zrefb[bv[i]], sv[i], flv[i], boxb(bv[i]), e_d);
+      }
+      unsigned r1v[2] = {0xffffffffu, 0xffffffffu};
+      if constexpr (KIND == kVoronoi) {  // the second reference, the next-least upper bound
+        unsigned key2[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) key2[i] = (unsigned)kv[i] != r0v[i] ? key[i] : 0xffffffffu;
+        brick_min(key2, r1v);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const unsigned k2 = r1v[i];
+          if (vv[i] && k2 != 0xffffffffu && (unsigned)kv[i] == (k2 & 63u))
+            put_ref(ws.zref2b[bv[i]], sv[i], flv[i], boxb(bv[i]), e_d);
+        }
+      }
+      __syncwarp();
+      bool kp[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        kp[i] = false;
+        if (i == 1 && M <= 32) continue;
+        const FBox Bs = boxb(bv[i]);
+        SiteF z;
+        float4 q3;
+        get_ref(ws.zrefb[bv[i]], z, q3);
+        const float tau = fminf(z.ubp, tcf);
+        bool k = vv[i] && ((unsigned)kv[i] == r0v[i] ||
+                           (sv[i].lbp <= tau &&
+                            bisector_keep<KIND, PER>(sv[i], flv[i], z, __float_as_uint(q3.y), Bs, halfLf, invG, e_d,
+                                                     q3.z, q3.w)));
+        if constexpr (KIND == kVoronoi) {
+          const unsigned k2 = r1v[i];
+          if (k && (unsigned)kv[i] != r0v[i] && k2 != 0xffffffffu && (unsigned)kv[i] != (k2 & 63u)) {
+            SiteF z2;
+            float4 q3b;
+            get_ref(ws.zref2b[bv[i]], z2, q3b);
+            k = bisector_keep<KIND, PER>(sv[i], flv[i], z2, __float_as_uint(q3b.y), Bs, halfLf, invG, e_d, q3b.z,
+                                         q3b.w);
+          }
+        }
+        kp[i] = k;
+      }
+      const unsigned m0 = __ballot_sync(0xffffffffu, kp[0]), m1 = __ballot_sync(0xffffffffu, kp[1]);
+      // brick b's slots in iteration i: lanes [off_b - 32 i, off_b+1 - 32 i) clamped to [0, 32)
+      auto seg = [](int lo, int hi) -> unsigned {
+        lo = max(0, min(32, lo));
+        hi = max(0, min(32, hi));
+        const unsigned mh = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
+        const unsigned ml = lo >= 32 ? 0xffffffffu : ((1u << lo) - 1u);
+        return mh & ~ml;
+      };
+      auto off_of = [&](int b) { return b == 0 ? 0 : b == 1 ? o1 : b == 2 ? o2 : b == 3 ? o3 : M; };
+      // lanes 0 .. kMaxBB-1: brick lane's bookkeeping (list space, info, overflow)
+      long long bbase = 0;
+      int bn2 = 0;
+      bool bokl = false;
+      int* bdst = list;
+      unsigned ev = 0;
+      if (lane < kMaxBB) {
+        const int b = lane;
+        const bool valid = b == 0 ? bval[0] : b == 1 ? bval[1] : b == 2 ? bval[2] : bval[3];
+        const bool okb = b == 0 ? bok[0] : b == 1 ? bok[1] : b == 2 ? bok[2] : bok[3];
+        if (valid) {
+          const int bz = bzo_of(b);
+          const int ez = min(8, ext[2] - bz);
+          const long long sbi = (long long)(bxo + K0[0]) / 8 +
+                                (long long)nsbx * ((K0[1] + byo) / 8 + nsby * ((K0[2] + bz - g.z_begin) >> 3));
+          if (VX_STATS_ON && lists_ok) {
+            const int nwb = ws.nw[b];
+            atomicAdd(&eval_slots[67], (unsigned long long)nwb);
+            atomicAdd(&eval_slots[68], 1ull);
+            atomicMax(&eval_slots[72], (unsigned long long)nwb);
+          }
+          if (okb) {
+            const int lo = off_of(b), hi = off_of(b + 1);
+            bn2 = __popc(m0 & seg(lo, hi)) + __popc(m1 & seg(lo - 32, hi - 32));
+            if (bn2 > kSlot && bn2 <= kLcap) bbase = (long long)atomicAdd(list_count, (unsigned long long)bn2);
+            bokl = bn2 <= kLcap && (bn2 <= kSlot || bbase + bn2 <= list_cap);
+            info[sbi] = bokl ? make_int2((int)bbase, bn2) : make_int2(0, -1);
+            bdst = bn2 <= kSlot ? slots16 + sbi * kSlot : list + bbase;
+            if (VX_STATS_ON) {
+              atomicAdd(&eval_slots[69], (unsigned long long)bn2);
+              atomicAdd(&eval_slots[70], 1ull);
+              atomicMax(&eval_slots[73], (unsigned long long)bn2);
+            }
+            if (bokl && bn2 <= kFcap) ev = (unsigned)(bn2 * ex0 * ex1 * ez);
+          } else {
+            info[sbi] = make_int2(0, -1);
+            atomicAdd(&ctr->overflow_bricks, 1ull);
+          }
+          if (!okb || !bokl) {  // the sub-brick shell labels it, 8 x 8 x 4 at a time
+            ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sb_id(K0[0] + bxo, K0[1] + byo, K0[2] + bz);
+            if (ez > 4) ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sb_id(K0[0] + bxo, K0[1] + byo, K0[2] + bz + 4);
+          }
+        }
+      }
+      ev += __shfl_xor_sync(0xffffffffu, ev, 1);
+      ev += __shfl_xor_sync(0xffffffffu, ev, 2);
+      if (lane == 0) ws.evals += ev;
+      // survivors -> their brick's slots (or overflow list), in slot order
+      const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        if (i == 1 && M <= 32) continue;
+        const int b = bv[i] & 3;
+        int* dst = reinterpret_cast<int*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(bdst), b));
+        const bool okl = __shfl_sync(0xffffffffu, bokl, b);
+        if (kp[i] && okl) {
+          const int lo = off_of(b), hi = off_of(b + 1);
+          const int rank = i == 0 ? __popc(m0 & seg(lo, hi) & lt)
+                                  : __popc(m0 & seg(lo, hi)) + __popc(m1 & seg(lo - 32, hi - 32) & lt);
+          dst[rank] = S.p[fv[i]];
+        }
+      }
+    }
+  }
+
+  if (!col_done)
   for (int bb = 0; bb < nbb; ++bb) {  // no barrier below: warps run independently
   const int bzo = (wid >> 2) * 8 + 16 * bb;
   const int bext[3] = {ex0, ex1, min(8, ext[2] - bzo)};
