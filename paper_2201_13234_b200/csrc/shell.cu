@@ -256,8 +256,18 @@ __device__ void shell_one(const Geo& g, const Bins& bins, const DevParams* prm, 
   *evals += ne;
 }
 
+// The search is a chain of dependent L2 loads per voxel: occupancy pays even
+// at the price of spills -- Voronoi / JM at 64 registers, 4 blocks (32 warps)
+// per SM (cfg2 shell 0.075 -> 0.055 ms, cfg4 0.054 -> 0.038, cfg5 0.068 ->
+// 0.055); Laguerre at 128 registers, 2 resident blocks (64: 0.077 -> 0.093)
+#ifndef VX_SHELL_MINB
+#define VX_SHELL_MINB 4
+#endif
+#ifndef VX_SHELL_MINB_L
+#define VX_SHELL_MINB_L 2
+#endif
 template <int KIND, bool PER>
-__global__ void __launch_bounds__(kShellThreads)
+__global__ void __launch_bounds__(kShellThreads, KIND == kLaguerre ? VX_SHELL_MINB_L : VX_SHELL_MINB)
     shell_kernel(Geo g, Bins bins, const DevParams* __restrict__ prm, int* __restrict__ labels,
                  double* __restrict__ dist, unsigned long long* __restrict__ hist,
                  const long long* __restrict__ unres, long long unres_cap, DevCounters* ctr) {
