@@ -1102,3 +1102,30 @@ def test_slab_window_binning_fallback_vs_oracle(oracle_mod, periodic):
         assert np.array_equal(bits(r.distances.values), bits(dist[a * plane: b * plane]))
         assert np.array_equal(r.histogram, np.bincount(ref, minlength=ns).astype(np.uint64))
         assert r.stats["n_unresolved"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spacing", [9.0, 12.0, 20.0])
+@pytest.mark.parametrize("kind,periodic", [(1, True), (1, False), (2, True), (2, False)])
+def test_column_brick_stage_vs_reference(spacing, kind, periodic):
+    """The timed kinds refine a warp's column of bricks in one pass when their
+    lists total <= 64 slots, else brick by brick; site spacings of 9 / 12 / 20
+    voxels put columns on both sides of that limit (and exercise single- and
+    two-slot lanes).  Bit-exact labels, distances and histogram against the
+    reference library."""
+    import oracle
+    import paper_2201_13234_b200 as vx
+
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    n = [144, 136, 160]
+    L = np.array([1.0, 136 / 144, 160 / 144])
+    ns = int(np.prod(n) / spacing ** 3)
+    pos, t = oracle.generate_uniform_sites(3, L, ns, kind, 0.5 * np.cbrt(np.prod(L) / ns), 77 + kind)
+    p = oracle.Problem(kind, n, L, periodic, pos, t, 1.0 if kind == 1 else 0.8)
+    lab_ref, dist_ref, _, _ = oracle.ref_tessellate(p)
+    sites, grid = to_vx(p)
+    r = vx.tessellate_fast(sites, grid, distances=True, histogram=True)
+    assert np.array_equal(r.labels.labels, lab_ref), int((r.labels.labels != lab_ref).sum())
+    assert np.array_equal(r.distances.values.view(np.uint64), dist_ref.view(np.uint64))
+    assert np.array_equal(r.histogram, np.bincount(lab_ref, minlength=ns).astype(np.uint64))
