@@ -940,8 +940,8 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz);
       if (BM && sext[2] > 4) ovf[atomicAdd(&ctr->n_ovf_sb, 1ull)] = (int)sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz + 4);
     };
-    auto list_id = [&](void) -> long long {
-      return BM ? (long long)(bxo + K0[0]) / 8 + (long long)nsbx * ((K0[1] + sy) / 8 + nsby * ((K0[2] + sz - g.z_begin) >> 3))
+    auto list_id = [&](void) -> long long {  // (K0 and the offsets are >= 0)
+      return BM ? ((K0[0] + bxo) >> 3) + nsbx * (((K0[1] + sy) >> 3) + nsby * ((K0[2] + sz - g.z_begin) >> 3))
                 : sb_id(K0[0] + bxo, K0[1] + sy, K0[2] + sz);
     };
     int n2 = 0;
@@ -1024,8 +1024,10 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       fbounds<KIND, PER>(S.rel[fa], fla, Bs, halfLf, invG, sa);
       if (vb) fbounds<KIND, PER>(S.rel[fb], flb, Bs, halfLf, invG, sb);
       // packed (upper bound, slot) arg-min -> reference s0 and tau = its ubp
+      // (Voronoi: ubp >= 0, whose bits already order as unsigned integers)
       auto okey = [](float v) -> unsigned {
         const unsigned b = __float_as_uint(v);
+        if (KIND == kVoronoi) return b;
         return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
       };
       unsigned km = min(va ? ((okey(sa.ubp) & ~63u) | (unsigned)lane) : 0xffffffffu,
@@ -1044,6 +1046,31 @@ __global__ void __launch_bounds__(kB2Threads, 4)
         zr[9] = o.t, zr[10] = o.lb, zr[11] = o.ub, zr[12] = o.ubp;
         zr[13] = __uint_as_float(rhi ? flb : fla);
         ref_consts(o, Bs, e_d, zr[14], zr[15]);
+      }
+      // Voronoi brick lists: a second reference, the next-least upper bound
+      // (cfg2 -2.4 %, cfg5 -1.6 %; JM / Laguerre spill with it), published
+      // before the same barrier as the first
+      bool two = false;
+      int r1 = 0;
+      if constexpr (KIND == kVoronoi && BM) {
+      unsigned km2 = min(va && lane != r0 ? ((okey(sa.ubp) & ~63u) | (unsigned)lane) : 0xffffffffu,
+                         vb && lane + 32 != r0 ? ((okey(sb.ubp) & ~63u) | (unsigned)(lane + 32)) : 0xffffffffu);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) km2 = min(km2, __shfl_xor_sync(0xffffffffu, km2, o));
+      two = km2 != 0xffffffffu;
+      r1 = (int)(km2 & 63u);
+      const int rl1 = r1 & 31;
+      const bool rhi1 = r1 >= 32;
+      if (two && lane == rl1) {
+        const SiteF& o = rhi1 ? sb : sa;
+        float* zr = ws.zref2;
+        zr[0] = o.v[0], zr[1] = o.v[1], zr[2] = o.v[2];
+        zr[3] = o.mn[0], zr[4] = o.mn[1], zr[5] = o.mn[2];
+        zr[6] = o.mx[0], zr[7] = o.mx[1], zr[8] = o.mx[2];
+        zr[9] = o.t, zr[10] = o.lb, zr[11] = o.ub, zr[12] = o.ubp;
+        zr[13] = __uint_as_float(rhi1 ? flb : fla);
+        ref_consts(o, Bs, e_d, zr[14], zr[15]);
+      }
       }
       __syncwarp();
       SiteF z;
@@ -1064,26 +1091,6 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       const float zZ2 = q3.z, zKz = q3.w;
       bool ka, kb;
       if constexpr (KIND == kVoronoi && BM) {
-      // Voronoi brick lists: a second reference, the next-least upper bound
-      // (cfg2 -2.4 %, cfg5 -1.6 %; JM / Laguerre spill with it)
-      unsigned km2 = min(va && lane != r0 ? ((okey(sa.ubp) & ~63u) | (unsigned)lane) : 0xffffffffu,
-                         vb && lane + 32 != r0 ? ((okey(sb.ubp) & ~63u) | (unsigned)(lane + 32)) : 0xffffffffu);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) km2 = min(km2, __shfl_xor_sync(0xffffffffu, km2, o));
-      const bool two = km2 != 0xffffffffu;
-      const int r1 = (int)(km2 & 63u), rl1 = r1 & 31;
-      const bool rhi1 = r1 >= 32;
-      if (two && lane == rl1) {
-        const SiteF& o = rhi1 ? sb : sa;
-        float* zr = ws.zref2;
-        zr[0] = o.v[0], zr[1] = o.v[1], zr[2] = o.v[2];
-        zr[3] = o.mn[0], zr[4] = o.mn[1], zr[5] = o.mn[2];
-        zr[6] = o.mx[0], zr[7] = o.mx[1], zr[8] = o.mx[2];
-        zr[9] = o.t, zr[10] = o.lb, zr[11] = o.ub, zr[12] = o.ubp;
-        zr[13] = __uint_as_float(rhi1 ? flb : fla);
-        ref_consts(o, Bs, e_d, zr[14], zr[15]);
-      }
-      __syncwarp();
       auto keep2 = [&](const SiteF& sx, unsigned flx, int slot) {
         if (!two || slot == r1) return true;
         SiteF z2;
