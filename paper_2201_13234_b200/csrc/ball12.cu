@@ -655,9 +655,17 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       tau[b] = bval[b] ? fminf(t, tcf) : __int_as_float(0xff800000);  // -inf: keeps nothing
       tlb[b] = KIND == kVoronoi ? tau[b] * ((1.f + 1e-6f) / (1.f - kRel)) : tau[b];
     }
+    // the lower-bound pass; standard lists: fused with the lists of every
+    // brick of the column (brick b in W[64 b, 64 b + 64)), in site-index
+    // order (dense mode: the mask bits to shared memory, lists per brick below)
     auto pass2 = [&](auto nb_tag) {
     constexpr int NB = decltype(nb_tag)::value;
-    for (int f = lane; f < T; f += 32) {
+    int nWb[kMaxBB] = {0, 0, 0, 0};
+    const unsigned lt = (1u << lane) - 1u;
+    for (int f0 = 0; f0 < T; f0 += 32) {
+      const int f = f0 + lane;
+      unsigned m = 0;
+      if (f < T) {
       const float4 s = S.rel[f];
       const unsigned fl = PER ? S.flag[f] : 0u;
       const float sx = PER && (fl & 1u) ? qnan : s.x;
@@ -666,7 +674,6 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       const float lx = fmaxf(fabsf(sx - Bxy.c[0]) - Bxy.h[0], 0.f);
       const float ly = fmaxf(fabsf(sy - Bxy.c[1]) - Bxy.h[1], 0.f);
       const float bxy = __fmaf_rn(ly, ly, lx * lx);
-      unsigned m = 0;
 #pragma unroll
       for (int b = 0; b < kMaxBB; ++b) {
         if (NB == 0 && b >= nbb) break;
@@ -677,33 +684,32 @@ __global__ void __launch_bounds__(kB2Threads, 4)
                                                     s.w - kRel * fabsf(s.w));
         if (lbp <= tlb[b]) m |= 1u << b;
       }
-      S.mk[wid][f] = (unsigned char)m;
+      if (DENSE) S.mk[wid][f] = (unsigned char)m;
+      }
+      if constexpr (!DENSE) {
+#pragma unroll
+        for (int b = 0; b < kMaxBB; ++b) {
+          if (NB == 0 && b >= nbb) break;
+          const bool keep = (m >> b) & 1u;
+          const unsigned bm = __ballot_sync(0xffffffffu, keep);
+          const int pos = nWb[b] + __popc(bm & lt);
+          if (keep && pos < kWcap) ws.W[b * kWcap + pos] = f;
+          nWb[b] += __popc(bm);
+        }
+      }
+    }
+    if (!DENSE && lane == 0) {
+#pragma unroll
+      for (int b = 0; b < kMaxBB; ++b) ws.nw[b] = nWb[b];
     }
     };
     if (nbb == kMaxBB) pass2(std::integral_constant<int, kMaxBB>{});
     else pass2(std::integral_constant<int, 0>{});
     __syncwarp();
-  }
-  // standard lists: every brick's list of the column in one pass over the
-  // gathered sites (brick b in W[64 b, 64 b + 64)), in site-index order
-  if (!DENSE && lists_ok) {
-    int nWb[kMaxBB] = {0, 0, 0, 0};
-    const unsigned lt = (1u << lane) - 1u;
-    for (int f0 = 0; f0 < T; f0 += 32) {
-      const int f = f0 + lane;
-      const unsigned m = f < T ? S.mk[wid][f] : 0u;
-#pragma unroll
-      for (int b = 0; b < kMaxBB; ++b) {
-        const bool keep = (m >> b) & 1u;
-        const unsigned bm = __ballot_sync(0xffffffffu, keep);
-        const int pos = nWb[b] + __popc(bm & lt);
-        if (keep && pos < kWcap) ws.W[b * kWcap + pos] = f;
-        nWb[b] += __popc(bm);
-      }
-    }
+  } else if (!DENSE && lists_ok) {  // no site reaches the super-brick: empty lists
     if (lane == 0) {
 #pragma unroll
-      for (int b = 0; b < kMaxBB; ++b) ws.nw[b] = nWb[b];
+      for (int b = 0; b < kMaxBB; ++b) ws.nw[b] = 0;
     }
     __syncwarp();
   }
