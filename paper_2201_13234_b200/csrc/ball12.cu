@@ -106,6 +106,7 @@ using EvalSmem = EvalSmemT<kFcap>;
 
 struct Smem2 {
   float4 rel[kTcap];   // (ux, uy, uz, t) relative to the super-brick centre
+  float4 reln[kTcap];  // periodic: the same with the ambiguous axes (flag bits 0..2) as NaN (column passes)
   int p[kTcap];        // binned position
   int idx[kTcap];      // original site index
   unsigned char flag[kTcap];  // bit a: periodic image ambiguous on axis a
@@ -521,9 +522,15 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       const unsigned rank = 4u * (unsigned)nk - ge;
       VXCHK(rank < (unsigned)T);
       // the kept sites move into site-index order
-      S.rel[rank] = S.g.rel[f];
+      const float4 rv = S.g.rel[f];
+      const unsigned fv = S.g.flag[f];
+      S.rel[rank] = rv;
       S.p[rank] = S.g.p[f];
-      S.flag[rank] = S.g.flag[f];
+      S.flag[rank] = (unsigned char)fv;
+      if (PER) {
+        const float qn = __int_as_float(0x7fffffff);
+        S.reln[rank] = make_float4(fv & 1u ? qn : rv.x, fv & 2u ? qn : rv.y, fv & 4u ? qn : rv.z, rv.w);
+      }
     }
   }
   __syncthreads();
@@ -612,7 +619,6 @@ __global__ void __launch_bounds__(kB2Threads, 4)
     // Voronoi the (1 + kRel) widening commutes with the minimum (RN(x c) is
     // monotone in x) and the lower-bound test lb (1 - kRel) <= tau is replaced
     // by the weaker lb <= tau / (1 - kRel) (1 + 1e-6): a superset is kept.
-    const float qnan = __int_as_float(0x7fffffff);
     float myub[kMaxBB];
 #pragma unroll
     for (int b = 0; b < kMaxBB; ++b) myub[b] = __int_as_float(0x7f800000);
@@ -620,11 +626,8 @@ __global__ void __launch_bounds__(kB2Threads, 4)
     auto pass1 = [&](auto nb_tag) {
     constexpr int NB = decltype(nb_tag)::value;
     for (int f = lane; f < T; f += 32) {
-      const float4 s = S.rel[f];
-      const unsigned fl = PER ? S.flag[f] : 0u;
-      const float sx = PER && (fl & 1u) ? qnan : s.x;
-      const float sy = PER && (fl & 2u) ? qnan : s.y;
-      const float sz = PER && (fl & 4u) ? qnan : s.z;
+      const float4 s = PER ? S.reln[f] : S.rel[f];  // NaN-coded ambiguous axes
+      const float sx = s.x, sy = s.y, sz = s.z;
       // no L/2 cap: on an unflagged axis |s - c| + h < L/2 already (up to the
       // widening, which only raises the bound), and a flagged (NaN) axis makes
       // the bound NaN, which fminf ignores -- a site left out of the minimum
@@ -666,11 +669,8 @@ __global__ void __launch_bounds__(kB2Threads, 4)
       const int f = f0 + lane;
       unsigned m = 0;
       if (f < T) {
-      const float4 s = S.rel[f];
-      const unsigned fl = PER ? S.flag[f] : 0u;
-      const float sx = PER && (fl & 1u) ? qnan : s.x;
-      const float sy = PER && (fl & 2u) ? qnan : s.y;
-      const float sz = PER && (fl & 4u) ? qnan : s.z;
+      const float4 s = PER ? S.reln[f] : S.rel[f];  // NaN-coded ambiguous axes
+      const float sx = s.x, sy = s.y, sz = s.z;
       const float lx = fmaxf(fabsf(sx - Bxy.c[0]) - Bxy.h[0], 0.f);
       const float ly = fmaxf(fabsf(sy - Bxy.c[1]) - Bxy.h[1], 0.f);
       const float bxy = __fmaf_rn(ly, ly, lx * lx);
