@@ -284,6 +284,10 @@ __device__ __forceinline__ void get_ref(const float* zr, SiteF& z, float4& q3) {
 }
 
 __device__ __forceinline__ long long wrapi2(long long c, long long m) {
+  // the gather windows are narrower than a period, so c lies in (-m, 2m):
+  // one conditional add or subtract (the 64-bit remainder is a ~70
+  // instruction subroutine); anything else takes the remainder
+  if (c >= -m && c < 2 * m) return c < 0 ? c + m : (c >= m ? c - m : c);
   const long long r = c % m;
   return r < 0 ? r + m : r;
 }
