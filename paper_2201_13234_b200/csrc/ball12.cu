@@ -1549,7 +1549,8 @@ __global__ void __launch_bounds__(32, KIND == kJohnsonMehl ? VX_EVAL16_MINB : VX
   const bool g1 = g.g_is_one;
 #pragma unroll kE16Unroll
   for (int j = 0; j < n2; ++j) {
-    const unsigned jj = (unsigned)j * 0x01010101u;
+    // packed slots hold byte offsets 4 j (< 128) into the int arrays Fidx / cnt
+    const unsigned jj = PACK ? (unsigned)j * 0x04040404u : (unsigned)j * 0x01010101u;
     const double wz0 = ws.T[j][16 + vz], wz1 = ws.T[j][20 + vz];
     const double wy0 = ws.T[j][8 + vy], wy1 = ws.T[j][12 + vy];
     const double a[4] = {__dadd_rn(wz0, wy0), __dadd_rn(wz0, wy1), __dadd_rn(wz1, wy0), __dadd_rn(wz1, wy1)};
@@ -1586,10 +1587,22 @@ __global__ void __launch_bounds__(32, KIND == kJohnsonMehl ? VX_EVAL16_MINB : VX
       }
     }
   }
-  if constexpr (PACK) {
-#pragma unroll
-    for (int k = 0; k < 16; ++k) bj[k] = (int)((bjp[k >> 2] >> (8 * (k & 3))) & 0xFFu);
-  }
+  // the winner's index / count slot of voxel k: packed, one PRMT (byte k & 3
+  // of bjp[k >> 2], zero-extended) gives the byte offset itself
+  auto fidx_of = [&](int k) -> int {
+    if constexpr (PACK)
+      return *reinterpret_cast<const int*>(reinterpret_cast<const char*>(ws.Fidx) +
+                                           __byte_perm(bjp[k >> 2], 0u, 0x4440u + (unsigned)(k & 3)));
+    else
+      return ws.Fidx[bj[k]];
+  };
+  auto cnt_of = [&](int k) -> int* {
+    if constexpr (PACK)
+      return reinterpret_cast<int*>(reinterpret_cast<char*>(ws.cnt) +
+                                    __byte_perm(bjp[k >> 2], 0u, 0x4440u + (unsigned)(k & 3)));
+    else
+      return &ws.cnt[bj[k]];
+  };
   // ---- resolve + store + compaction ----
   const int xr = bext[0] - qx;
   const unsigned xm = xr >= 4 ? 0xFu : (xr > 0 ? (1u << xr) - 1u : 0u);
@@ -1613,8 +1626,8 @@ __global__ void __launch_bounds__(32, KIND == kJohnsonMehl ? VX_EVAL16_MINB : VX
       lab[k] = -1;
       if (FULL || ((vmask >> k) & 1u)) {
         if (best[k] <= cutoff) {
-          lab[k] = ws.Fidx[bj[k]];
-          if (hist) atomicAdd(&ws.cnt[bj[k]], 1);
+          lab[k] = fidx_of(k);
+          if (hist) atomicAdd(cnt_of(k), 1);
         } else {
           umask |= 1u << k;
         }
@@ -1629,8 +1642,8 @@ __global__ void __launch_bounds__(32, KIND == kJohnsonMehl ? VX_EVAL16_MINB : VX
     // straight-line label lookups and histogram counts
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-      lab[k] = ws.Fidx[bj[k]];
-      if (hist) atomicAdd(&ws.cnt[bj[k]], 1);
+      lab[k] = fidx_of(k);
+      if (hist) atomicAdd(cnt_of(k), 1);
     }
   } else if (vmask == 0xFFFFu) {
     resolve(std::true_type{});
