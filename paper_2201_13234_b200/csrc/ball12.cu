@@ -1441,7 +1441,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 32 / kEvalWarps)
 // of eval12.  Same exact arithmetic, ascending-index strict-< scan, resolve,
 // stores, histogram and compaction.
 struct __align__(16) Eval16Smem {
-  double T[kFcap][24]; // exact w^2: [0,8) x, [8,16) y, [16,24) z
+  double T[kFcap][24]; // exact w^2: [0,8) x, [8,16) y, [16,24) z (Voronoi / Laguerre: y, z in the order 0 4 1 5 2 6 3 7)
   double C[24];
   double Ft[kFcap];
   int P[kFcap];
@@ -1505,8 +1505,12 @@ __global__ void __launch_bounds__(32, KIND == kJohnsonMehl ? VX_EVAL16_MINB : VX
     if (KIND != kVoronoi) ws.Ft[lane] = bins.t[pl];
   }
   if (lane < 24 && n2 > 0) {  // the brick's voxel centres (geometry.hpp:58-60)
-    const int a = lane >> 3;
-    const int k = min(lane & 7, (a == 0 ? bext[0] : (a == 1 ? bext[1] : bext[2])) - 1);
+    // y and z in the order 0 4 1 5 2 6 3 7, so a lane's two rows / planes
+    // (v, v + 4) are adjacent in the tables (one 16-byte load each); the
+    // first and last entries stay the extremes the wrap test looks at
+    const int a = lane >> 3, s8 = lane & 7;
+    const int kk = a == 0 || KIND == kJohnsonMehl ? s8 : (s8 >> 1) + 4 * (s8 & 1);  // JM: natural order (+1.4 % interleaved)
+    const int k = min(kk, (a == 0 ? bext[0] : (a == 1 ? bext[1] : bext[2])) - 1);
     const long long k0 = a == 0 ? (long long)x0 : (a == 1 ? (long long)y0 : z0);
     ws.C[lane] = center(k0 + k, a == 0 ? g.sp[0] : (a == 1 ? g.sp[1] : g.sp[2]));
   }
@@ -1551,8 +1555,15 @@ __global__ void __launch_bounds__(32, KIND == kJohnsonMehl ? VX_EVAL16_MINB : VX
   for (int j = 0; j < n2; ++j) {
     // packed slots hold byte offsets 4 j (< 128) into the int arrays Fidx / cnt
     const unsigned jj = PACK ? (unsigned)j * 0x04040404u : (unsigned)j * 0x01010101u;
-    const double wz0 = ws.T[j][16 + vz], wz1 = ws.T[j][20 + vz];
-    const double wy0 = ws.T[j][8 + vy], wy1 = ws.T[j][12 + vy];
+    double wz0, wz1, wy0, wy1;
+    if constexpr (KIND != kJohnsonMehl) {
+      const double2 wz = *reinterpret_cast<const double2*>(&ws.T[j][16 + 2 * vz]);  // planes vz, vz + 4
+      const double2 wy = *reinterpret_cast<const double2*>(&ws.T[j][8 + 2 * vy]);   // rows vy, vy + 4
+      wz0 = wz.x, wz1 = wz.y, wy0 = wy.x, wy1 = wy.y;
+    } else {
+      wz0 = ws.T[j][16 + vz], wz1 = ws.T[j][20 + vz];
+      wy0 = ws.T[j][8 + vy], wy1 = ws.T[j][12 + vy];
+    }
     const double a[4] = {__dadd_rn(wz0, wy0), __dadd_rn(wz0, wy1), __dadd_rn(wz1, wy0), __dadd_rn(wz1, wy1)};
     const double2 w01 = *reinterpret_cast<const double2*>(&ws.T[j][qx]);
     const double2 w23 = *reinterpret_cast<const double2*>(&ws.T[j][qx + 2]);
