@@ -1,6 +1,6 @@
 """Small instances through every engine path, for compute-sanitizer runs:
 3-D (standard, dense mode, overflow -> sub-brick shell, slab window with the
-all-sites fallback), d != 3 (1, 2, 4, 6), timed kinds with prune, the brute
+all-sites fallback, the timed kinds' column brick stage at ~9-voxel spacing), d != 3 (1, 2, 4, 6), timed kinds with prune, the brute
 engine and validate_partition.  python scripts/sanitize_cases.py"""
 import os
 import sys
@@ -16,7 +16,7 @@ from conftest import to_vx  # noqa: E402
 
 rng = np.random.default_rng(3)
 cases = []
-for d, counts, ns in ((3, [40, 33, 29], 300), (3, [48, 40, 36], 6000), (3, [30, 30, 200], 40),
+for d, counts, ns in ((3, [40, 33, 29], 300), (3, [48, 40, 36], 6000), (3, [30, 30, 200], 40), (3, [72, 64, 80], 500),
                       (1, [3000], 200), (2, [90, 70], 900), (4, [9, 8, 10, 7], 300), (6, [4, 5, 3, 4, 5, 4], 200)):
     for kind in (0, 1, 2):
         for per in (True, False):
