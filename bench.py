@@ -489,6 +489,7 @@ def run_ours(args):
         out = torch.empty(nvs, dtype=torch.int32).pin_memory().numpy()
         hist_h = torch.zeros(ns, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
         e2e_t = []
+        d2h_bytes = []
         for k in range(1 + args.e2e_steps):
             if dist is not None:
                 dist.barrier()
@@ -496,13 +497,17 @@ def run_ours(args):
             r = vx.tessellate_fast(sites_h, grid, distances=False, histogram=True, slab=(zb, ze),
                                    device=dev, out=out, histogram_out=hist_h)
             e2e_t.append(time.perf_counter() - t0)
+            d2h_bytes.append(int(_lib.lib().vx_last_d2h_bytes()))
         t_e2e = torch.tensor([float(np.mean(e2e_t[1:]))], dtype=torch.float64, device=f"cuda:{dev}")
         if dist is not None:
             dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
         e2e = {"value": nv_total / float(t_e2e.item()) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(sites.positions.nbytes +
                                          (sites.times.nbytes if sites.times is not None else 0)),
-               "d2h_bytes_per_step": int(4 * nvs + 8 * ns),
+               # counted by the library: the label image crosses PCIe as runs
+               # of equal labels along x (expanded into `out` on host threads)
+               "d2h_bytes_per_step": int(np.mean(d2h_bytes[1:])),
+               "d2h_raw_bytes_per_step": int(4 * nvs + 8 * ns),
                "ms_per_step": float(t_e2e.item()) * 1e3, "host_buffers": "pinned"}
         if world == 1:
             fp = "%016x" % _lib.lib().vx_label_fingerprint(out.ctypes.data_as(_lib.C.c_void_p), out.size)

@@ -132,6 +132,14 @@ uint32_t vx_abi_version(void);
 const char* vx_version_string(void);
 /* thread-local message of the last failing call on this thread */
 const char* vx_last_error(void);
+/* Bytes the calling thread's last vx_tessellate call moved device -> host
+ * (host-buffer calls: label image, distances, histogram).  Synchronous 3-D
+ * host-buffer calls without distances move the label image as runs of equal
+ * labels along x (per x-row an 8-byte record, per run an int32 label and a
+ * uint16 first x) and expand them into labels_out on host threads; chunks
+ * whose runs average < 4 voxels are copied raw.  labels_out is identical
+ * either way.  VX_D2H_RAW=1 forces the raw copy. */
+uint64_t vx_last_d2h_bytes(void);
 void vx_options_init(vx_options* opt);
 
 /* ---- contexts: own a device, a stream and cached workspaces ---- */

@@ -94,6 +94,7 @@ SIGNATURES = {
     "vx_abi_version": (C.c_uint32, []),
     "vx_version_string": (C.c_char_p, []),
     "vx_last_error": (C.c_char_p, []),
+    "vx_last_d2h_bytes": (C.c_uint64, []),
     "vx_options_init": (None, [C.POINTER(vx_options)]),
     "vx_context_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "vx_context_destroy": (None, [_P]),

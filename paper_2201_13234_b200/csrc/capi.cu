@@ -25,6 +25,8 @@
 #include <string>
 #include <thread>
 #include <chrono>
+#include <condition_variable>
+#include <cstdlib>
 #include <vector>
 
 #include "voxellate_b200.h"
@@ -35,6 +37,7 @@ using namespace vxb;
 namespace {
 
 thread_local std::string g_err;
+thread_local uint64_t g_d2h_bytes = 0;  // vx_last_d2h_bytes
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -79,7 +82,8 @@ struct vx_context {
   std::mutex mu;
   Buf pos_raw, t_raw, w_raw, p3, t, dropped, keys_a, keys_b, vals_a, vals_b, bx, by, bz, bt, bidx,
       cell_start, cub, labels, dist, hist, unres, params, counters, scratch, vsample, vlab, vdist,
-      vbad, slots, f4, sb_info, sb_list, sb_count, sb_slots, sb_ovf, ctab, nd_x, nd_t, nd_idx, nd_cells, cell_fill;
+      vbad, slots, f4, sb_info, sb_list, sb_count, sb_slots, sb_ovf, ctab, nd_x, nd_t, nd_idx, nd_cells, cell_fill,
+      rc_rows, rc_lab, rc_x, rc_cnt;
   DevParams* h_prm = nullptr;
   DevCounters* h_ctr = nullptr;
   cudaEvent_t ev[8] = {};  // stage markers (options.profile_stages)
@@ -92,6 +96,8 @@ struct vx_context {
   cudaEvent_t done_ev[2] = {};
   void* pin[2] = {};                   // pinned double buffer of the file writer
   size_t pin_bytes = 0;
+  void* rc_pin = nullptr;              // pinned landing area of the run-coded label transport
+  size_t rc_pin_bytes = 0;
 
   vx_context() = default;
   vx_context(const vx_context&) = delete;
@@ -100,11 +106,12 @@ struct vx_context {
   // default contexts when their thread exits, and a failed create_context.
   ~vx_context();
 
-  Buf* all[41] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
+  Buf* all[45] = {&pos_raw, &t_raw,   &w_raw, &p3,    &t,      &dropped, &keys_a,   &keys_b,
                   &vals_a,  &vals_b,  &bx,    &by,    &bz,     &bt,      &bidx,     &cell_start,
                   &cub,     &labels,  &dist,  &hist,  &unres,  &params,  &counters, &scratch,
                   &vsample, &vlab,    &vdist, &vbad,  &slots,  &f4,      &sb_info,  &sb_list,
-                  &sb_count, &sb_slots, &sb_ovf, &ctab, &nd_x,  &nd_t,   &nd_idx,   &nd_cells, &cell_fill};
+                  &sb_count, &sb_slots, &sb_ovf, &ctab, &nd_x,  &nd_t,   &nd_idx,   &nd_cells, &cell_fill,
+                  &rc_rows, &rc_lab, &rc_x, &rc_cnt};
 };
 
 namespace {
@@ -152,6 +159,7 @@ vx_context::~vx_context() {
     if (e) cudaEventDestroy(e);
   for (auto b : pin)
     if (b) cudaFreeHost(b);
+  if (rc_pin) cudaFreeHost(rc_pin);
   for (auto e : ev)
     if (e) cudaEventDestroy(e);
   if (handoff_ev) cudaEventDestroy(handoff_ev);
@@ -454,6 +462,166 @@ cudaEvent_t sink_event(vx_context* ctx, size_t i, cudaStream_t st) {
   return ctx->sink_ev[i];
 }
 
+// ---- run-coded label transport (labelrun.cu) ----
+// One z-chunk of a host-buffer call: its x-rows [r0, r0 + rows) of the slab,
+// its run region [b0, b0 + cap) of the run arrays.
+struct RunChunk {
+  long long r0, rows, b0, cap;
+};
+
+struct RunPlan {
+  int2* rows = nullptr;  // device
+  int* lab = nullptr;
+  unsigned short* x = nullptr;
+  unsigned long long* cnt = nullptr;
+  int2* p_rows = nullptr;  // pinned mirrors
+  int* p_lab = nullptr;
+  unsigned short* p_x = nullptr;
+  unsigned long long* p_cnt = nullptr;  // mapped: written by launch_run_publish
+  unsigned long long* d_pcnt = nullptr;  // its device address
+  std::vector<RunChunk> chunks;
+  std::vector<cudaEvent_t> enc, d2h;  // encoded (call stream), copied (copy stream)
+  ~RunPlan() {
+    for (auto e : enc) cudaEventDestroy(e);
+    for (auto e : d2h) cudaEventDestroy(e);
+  }
+};
+
+// Device and pinned buffers for a slab of nvs voxels in rows of n0, nck chunks.
+void run_plan_init(vx_context* ctx, RunPlan& rp, int64_t nvs, int64_t n0, int nck) {
+  const size_t nrows = (size_t)(nvs / n0), cap = (size_t)(nvs / 4);
+  rp.rows = ensure<int2>(ctx->rc_rows, nrows);
+  rp.lab = ensure<int>(ctx->rc_lab, cap);
+  rp.x = ensure<unsigned short>(ctx->rc_x, cap);
+  rp.cnt = ensure<unsigned long long>(ctx->rc_cnt, (size_t)nck);
+  auto up = [](size_t b) { return (b + 63) / 64 * 64; };
+  const size_t o_lab = up(nrows * sizeof(int2)), o_x = o_lab + up(cap * 4), o_cnt = o_x + up(cap * 2);
+  const size_t bytes = o_cnt + up((size_t)nck * 8);
+  if (ctx->rc_pin_bytes < bytes) {
+    if (ctx->rc_pin) cudaFreeHost(ctx->rc_pin);
+    ctx->rc_pin = nullptr;
+    ctx->rc_pin_bytes = 0;
+    ck(cudaHostAlloc(&ctx->rc_pin, bytes, cudaHostAllocMapped), "cudaHostAlloc (label runs)");
+    ctx->rc_pin_bytes = bytes;
+  }
+  char* b = static_cast<char*>(ctx->rc_pin);
+  rp.p_rows = reinterpret_cast<int2*>(b);
+  rp.p_lab = reinterpret_cast<int*>(b + o_lab);
+  rp.p_x = reinterpret_cast<unsigned short*>(b + o_x);
+  rp.p_cnt = reinterpret_cast<unsigned long long*>(b + o_cnt);
+  ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&rp.d_pcnt), rp.p_cnt, 0), "mapped run counts");
+  for (int i = 0; i < nck; ++i) {
+    cudaEvent_t e1, e2;
+    ck(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming | cudaEventBlockingSync), "event");
+    rp.enc.push_back(e1);
+    ck(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming | cudaEventBlockingSync), "event");
+    rp.d2h.push_back(e2);
+  }
+}
+
+// Host side of the transport: as each chunk's runs are coded, copy them (or,
+// when they exceed the chunk's cap, its raw labels) to the host on the copy
+// stream; T host threads expand every copied chunk into `out` while the next
+// one is in flight.  Returns the bytes moved device -> host.
+uint64_t run_drain(vx_context* ctx, RunPlan& rp, const int32_t* d_labels, int32_t* out, int n0) {
+  const int nck = (int)rp.chunks.size();
+  int T = (int)std::thread::hardware_concurrency();
+  if (const char* e = std::getenv("VX_D2H_THREADS")) T = std::atoi(e);
+  T = std::max(1, std::min(T, 64));
+  std::vector<int> mode(nck, 0);  // 1: raw copy, 2: runs
+  // VX_RUN_TRACE=1: per chunk, ms since the drain started when its runs were
+  // coded, copied and (thread 0's share) expanded
+  const bool rtrace = std::getenv("VX_RUN_TRACE") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  auto ms_now = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(); };
+  std::vector<double> t_enc(nck), t_cp(nck), t_dec(nck);
+  std::mutex mu;
+  std::condition_variable cv;
+  int issued = 0;
+  bool failed = false;
+  auto worker = [&](int t) {
+    std::vector<int> buf;
+    for (int c = 0; c < nck; ++c) {
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return issued > c || failed; });
+        if (failed) return;
+      }
+      if (mode[c] != 2) continue;
+      if (cudaEventSynchronize(rp.d2h[c]) != cudaSuccess) {
+        std::lock_guard<std::mutex> lk(mu);
+        failed = true;
+        cv.notify_all();
+        return;
+      }
+      if (rtrace && t == 0) t_cp[c] = ms_now();
+      const RunChunk& k = rp.chunks[c];
+      run_decode_rows(reinterpret_cast<const int*>(rp.p_rows + k.r0), rp.p_lab + k.b0, rp.p_x + k.b0, k.rows * t / T, k.rows * (t + 1) / T, n0,
+                      out + k.r0 * n0, buf);
+      if (rtrace && t == 0) t_dec[c] = ms_now();
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 0; t < T; ++t) th.emplace_back(worker, t);
+  uint64_t bytes = 0;
+  auto stop = [&] {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      failed = true;
+    }
+    cv.notify_all();
+    for (auto& x : th) x.join();
+  };
+  try {
+    for (int c = 0; c < nck; ++c) {
+      const RunChunk& k = rp.chunks[c];
+      ck(cudaEventSynchronize(rp.enc[c]), "label runs");
+      if (rtrace) t_enc[c] = ms_now();
+      const unsigned long long n = reinterpret_cast<volatile unsigned long long*>(rp.p_cnt)[c];
+      int m = 2;
+      if (n <= (unsigned long long)k.cap) {
+        ck(cudaMemcpyAsync(rp.p_rows + k.r0, rp.rows + k.r0, sizeof(int2) * k.rows, cudaMemcpyDeviceToHost,
+                           ctx->copy_stream), "D2H label runs");
+        ck(cudaMemcpyAsync(rp.p_lab + k.b0, rp.lab + k.b0, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->copy_stream),
+           "D2H label runs");
+        ck(cudaMemcpyAsync(rp.p_x + k.b0, rp.x + k.b0, sizeof(unsigned short) * n, cudaMemcpyDeviceToHost,
+                           ctx->copy_stream), "D2H label runs");
+        bytes += sizeof(int2) * k.rows + 6 * n + 8;
+      } else {  // short runs: the chunk's labels as they are
+        m = 1;
+        ck(cudaMemcpyAsync(out + k.r0 * n0, d_labels + k.r0 * n0, sizeof(int32_t) * k.rows * n0,
+                           cudaMemcpyDeviceToHost, ctx->copy_stream), "D2H labels");
+        bytes += sizeof(int32_t) * k.rows * n0 + 8;
+      }
+      ck(cudaEventRecord(rp.d2h[c], ctx->copy_stream), "copy event");
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        mode[c] = m;
+        issued = c + 1;
+      }
+      cv.notify_all();
+    }
+    for (auto& x : th) x.join();
+    th.clear();
+    bool bad = false;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      bad = failed;
+    }
+    ck(cudaStreamSynchronize(ctx->copy_stream), "D2H labels");
+    if (bad) ck(cudaErrorUnknown, "label runs");
+    if (rtrace) {
+      fprintf(stderr, "VX_RUN_TRACE %d threads, %d chunks, %.1f ms:", T, nck, ms_now());
+      for (int c = 0; c < nck; ++c) fprintf(stderr, " [%d %s enc %.1f cp %.1f dec %.1f]", c, mode[c] == 2 ? "runs" : "raw", t_enc[c], t_cp[c], t_dec[c]);
+      fprintf(stderr, "\n");
+    }
+  } catch (...) {
+    if (!th.empty()) stop();
+    throw;
+  }
+  return bytes;
+}
+
 struct FileSink;
 int write_sink(vx_context* ctx, const vx_problem* P, const FileSink& sink, const std::vector<SinkChunk>& chunks,
                const int32_t* lab, const double* dist, int64_t zb, int64_t plane);
@@ -690,6 +858,8 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
   const int64_t ns = P->n_sites;
   StageTimer tm;
   bool labels_copied = false;  // chunked D2H already issued
+  RunPlan rp;                  // run-coded label transport of this call
+  bool run_pending = false;    // its chunks still to be copied and expanded
   std::vector<SinkChunk> sink_chunks;
   try {
     // asynchronous calls (and CUDA-graph captures of them) record the stage
@@ -928,10 +1098,16 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       // computed (the PCIe copy of the label image is the larger cost of such a
       // call).  Chunks are whole super-bricks of the ball kernel (64 planes).
       const int64_t nz = ze - zb;
+      // run-coded label transport (labelrun.cu): synchronous host-buffer
+      // calls of 3-D images, labels only, rows of 64..65535 voxels
+      bool rle = host_io && !tm.on && (sink == nullptr || sink == &mem_sink) && !want_dist && !O.asynchronous &&
+                 d == 3 && !xy2d && g.n[0] >= 64 && g.n[0] <= 65535 && (size_t)nvs * 4 >= (16u << 20) &&
+                 nvs / 4 < (1ll << 31) && std::getenv("VX_D2H_RAW") == nullptr;
+      if (rle) sink = nullptr;  // pageable output: the decode threads write it directly
       int nchunk = 1;
       if (host_io && !tm.on && !sink) {
         const char* e = std::getenv("VX_CHUNKS");
-        nchunk = e ? std::max(1, std::min(kMaxChunks, std::atoi(e))) : (nz >= 256 ? 8 : 1);
+        nchunk = e ? std::max(1, std::min(kMaxChunks, std::atoi(e))) : (nz >= 256 ? (rle ? 16 : 8) : 1);
       }
       int64_t cz = nchunk > 1 ? ((nz + nchunk - 1) / nchunk + 63) / 64 * 64 : nz;
       const bool pipelined = nchunk > 1;  // chunk D2H overlaps the next chunk's compute
@@ -943,7 +1119,8 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       // the ball kernels put the last axis in gridDim.z (<= 65535 of 4..64
       // planes each): longer slabs are labelled in several launches
       cz = std::min<int64_t>(cz, kMaxZPlanes);
-      if (pipelined && !ctx->copy_stream) {
+      if (rle) run_plan_init(ctx, rp, nvs, g.n[0], (int)((nz + cz - 1) / cz));
+      if ((pipelined || rle) && !ctx->copy_stream) {
         ck(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
         for (auto& e : ctx->chunk_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
       }
@@ -961,7 +1138,15 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
         ball_and_shell(gc, lb, ds);
         if (sink) sink_chunks.push_back({c0, c1, sink_event(ctx, ci, st)});
         if (ci == 0) trace.rec(1, st);
-        if (pipelined) {
+        if (rle) {
+          const RunChunk k{(c0 - zb) * plane / g.n[0], (c1 - c0) * plane / g.n[0], (c0 - zb) * plane / 4,
+                           (c1 - c0) * plane / 4};
+          launches += launch_run_encode(lb, k.rows, (int)g.n[0], rp.rows + k.r0, rp.lab + k.b0, rp.x + k.b0, k.cap,
+                                        rp.cnt + ci, st);
+          launches += launch_run_publish(rp.cnt + ci, rp.d_pcnt + ci, st);
+          ck(cudaEventRecord(rp.enc[ci], st), "run event");
+          rp.chunks.push_back(k);
+        } else if (pipelined) {
           cudaEvent_t ev = ctx->chunk_ev[ci % kMaxChunks];
           ck(cudaEventRecord(ev, st), "chunk event");
           ck(cudaStreamWaitEvent(ctx->copy_stream, ev, 0), "chunk wait");
@@ -975,7 +1160,10 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
         }
       }
       trace.rec(2, st);
-      if (pipelined) {  // the call's stream waits for the last copy
+      if (rle) {
+        labels_copied = true;
+        run_pending = true;
+      } else if (pipelined) {  // the call's stream waits for the last copy
         trace.rec(3, ctx->copy_stream);
         ck(cudaEventRecord(ctx->chunk_ev[ci % kMaxChunks], ctx->copy_stream), "copy event");
         ck(cudaStreamWaitEvent(st, ctx->chunk_ev[ci % kMaxChunks], 0), "copy wait");
@@ -999,6 +1187,9 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
         ck(cudaMemcpyAsync(O.histogram_out, hist, sizeof(unsigned long long) * ns,
                            cudaMemcpyDeviceToHost, st),
            "D2H histogram");
+      g_d2h_bytes = (uint64_t)(hist ? 8 * ns : 0) +
+                    (run_pending ? run_drain(ctx, rp, lab, labels_out, (int)P->counts[0])
+                                 : (uint64_t)nvs * (dist ? 12 : 4));
     }
     tm.mark(6);
     if (stats) {
@@ -1173,6 +1364,7 @@ const char* vx_version_string(void) {
 }
 
 const char* vx_last_error(void) { return g_err.c_str(); }
+uint64_t vx_last_d2h_bytes(void) { return g_d2h_bytes; }
 
 void vx_options_init(vx_options* o) {
   if (!o) return;
@@ -1217,6 +1409,7 @@ int64_t vx_context_workspace_bytes(const vx_context* ctx) {
 
 int vx_tessellate(vx_context* ctx, const vx_problem* problem, const vx_options* options,
                   int32_t* labels_out, vx_stats* stats_out) {
+  g_d2h_bytes = 0;
   if (options && options->n_gpus > 1) return run_multi(problem, *options, labels_out, stats_out, false);
   return run(ctx, problem, options, labels_out, stats_out, false);
 }

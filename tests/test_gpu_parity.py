@@ -480,6 +480,77 @@ def test_chunked_host_copies_identical(kind):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("case", ["sparse", "dense", "mixed", "odd_rows", "jm_np"])
+def test_run_coded_transport_identical(case):
+    """Synchronous 3-D host-buffer calls move the label image across PCIe as
+    runs along x and expand them on host threads (labelrun.cu); chunks whose
+    runs average < 4 voxels go raw.  The caller's image (pinned or pageable,
+    any chunking) must equal the raw transport's and the device-pointer
+    call's, voxel for voxel."""
+    import torch
+    import paper_2201_13234_b200 as vx
+    from paper_2201_13234_b200 import _lib
+
+    rng = np.random.default_rng({"sparse": 1, "dense": 2, "mixed": 3, "odd_rows": 4, "jm_np": 5}[case])
+    kind, periodic = (1, False) if case == "jm_np" else (0, True)
+    counts = {"odd_rows": [101, 130, 320]}.get(case, [160, 96, 300])
+    L = np.array([1.0, 0.6, 1.9]) if case != "odd_rows" else np.array([1.0, 1.3, 3.1])
+    nv = int(np.prod(counts))
+    if case == "dense":
+        ns = nv // 3
+        pos = rng.uniform(0, 1, (ns, 3)) * L
+    elif case == "mixed":  # dense near z = 0 (raw chunks), sparse above (runs)
+        a = rng.uniform(0, 1, (nv // 6, 3)) * L * np.array([1, 1, 0.2])
+        b = rng.uniform(0, 1, (2000, 3)) * L * np.array([1, 1, 0.8]) + np.array([0, 0, 0.2 * L[2]])
+        pos = np.concatenate([a, b])
+        ns = len(pos)
+    else:
+        ns = 3000
+        pos = rng.uniform(0, 1, (ns, 3)) * L
+    pos = np.ascontiguousarray(np.minimum(pos, np.nextafter(L, 0)))
+    t = rng.uniform(0, 0.05, ns) if kind == 1 else None
+    box = vx.Domain(list(L), vx.Boundary.Periodic if periodic else vx.Boundary.NonPeriodic)
+    grid = vx.VoxelGrid(counts, box)
+    sites = vx.SiteSet(vx.Kind(kind), 3, pos, t, 1.0 if kind else 0.0)
+    old = {k: os.environ.get(k) for k in ("VX_D2H_RAW", "VX_CHUNKS")}
+    res = {}
+    try:
+        os.environ["VX_D2H_RAW"] = "1"
+        res["raw"] = vx.tessellate_fast(sites, grid, distances=False).labels.labels.copy()
+        raw_bytes = int(_lib.lib().vx_last_d2h_bytes())
+        os.environ.pop("VX_D2H_RAW")
+        for ch in ("1", "5", "8"):
+            os.environ["VX_CHUNKS"] = ch
+            out = torch.empty(nv, dtype=torch.int32).pin_memory().numpy()
+            vx.tessellate_fast(sites, grid, distances=False, out=out)
+            res["pinned" + ch] = out.copy()
+            res["pageable" + ch] = vx.tessellate_fast(sites, grid, distances=False).labels.labels.copy()
+            run_bytes = int(_lib.lib().vx_last_d2h_bytes())
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert raw_bytes == 4 * nv
+    for k, v in res.items():
+        assert np.array_equal(v.reshape(-1), res["raw"].reshape(-1)), k
+    if case == "dense":
+        assert run_bytes >= 4 * nv  # every chunk raw
+    else:
+        assert run_bytes < 4 * nv * (0.8 if case == "mixed" else 0.5)
+    # and the raw image itself against the device-pointer path
+    from paper_2201_13234_b200.engine import Tessellator
+
+    eng = Tessellator(0)
+    lab_d = torch.empty(nv, dtype=torch.int32, device="cuda")
+    eng.run(kind=kind, counts=counts, lengths=list(L), periodic=periodic, positions=torch.from_numpy(pos).cuda(),
+            labels=lab_d, times=None if t is None else torch.from_numpy(t).cuda(), growth=1.0 if kind else 0.0)
+    assert np.array_equal(lab_d.cpu().numpy().view(np.uint32), res["raw"].reshape(-1).view(np.uint32))
+    eng.close()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("case", ["vor3d", "jm3d_dist", "lag2d", "brute4d"])
 def test_tessellate_to_files_streams_the_image(case, tmp_path):
     """vx_tessellate_to_files streams each z-chunk of the image from device
