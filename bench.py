@@ -601,7 +601,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="per-step C-ABI calls instead of CUDA-graph replays")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     # functional dry run of the N > 1 path on a one-GPU box (not a measurement):
     # gloo collectives, every rank on cuda:0
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"], help=argparse.SUPPRESS)

@@ -525,7 +525,10 @@ void run_plan_init(vx_context* ctx, RunPlan& rp, int64_t nvs, int64_t n0, int nc
 // one is in flight.  Returns the bytes moved device -> host.
 uint64_t run_drain(vx_context* ctx, RunPlan& rp, const int32_t* d_labels, int32_t* out, int n0) {
   const int nck = (int)rp.chunks.size();
-  int T = (int)std::thread::hardware_concurrency();
+  // one hardware thread stays free for this (issuing) thread: it must wake
+  // promptly when a chunk is coded, and busy expanders would delay it by a
+  // scheduler slice
+  int T = (int)std::thread::hardware_concurrency() - 1;
   if (const char* e = std::getenv("VX_D2H_THREADS")) T = std::atoi(e);
   T = std::max(1, std::min(T, 64));
   std::vector<int> mode(nck, 0);  // 1: raw copy, 2: runs
