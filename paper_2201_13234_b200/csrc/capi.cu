@@ -528,7 +528,14 @@ uint64_t run_drain(vx_context* ctx, RunPlan& rp, const int32_t* d_labels, int32_
   // one hardware thread stays free for this (issuing) thread: it must wake
   // promptly when a chunk is coded, and busy expanders would delay it by a
   // scheduler slice
-  int T = (int)std::thread::hardware_concurrency() - 1;
+  // concurrent drains (one per device of an n_gpus call) share the cores
+  static std::atomic<int> active{0};
+  struct Active {
+    int n;
+    Active() : n(++active) {}
+    ~Active() { --active; }
+  } act;
+  int T = ((int)std::thread::hardware_concurrency() - act.n) / act.n;
   if (const char* e = std::getenv("VX_D2H_THREADS")) T = std::atoi(e);
   T = std::max(1, std::min(T, 64));
   std::vector<int> mode(nck, 0);  // 1: raw copy, 2: runs
