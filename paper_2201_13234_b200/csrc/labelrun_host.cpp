@@ -23,6 +23,18 @@ __attribute__((target("avx512f"))) void fill_row_avx512(const int* L, const unsi
   }
 }
 
+// b -> out (out 16-byte aligned, n0 % 4 == 0): 16-byte streaming stores up
+// to the first 64-byte boundary, whole-line streaming stores, then the tail.
+__attribute__((target("avx512f"))) void stream_row_avx512(int32_t* out, const int* b, int n0) {
+  int x = 0;
+  for (; x < n0 && (reinterpret_cast<uintptr_t>(out + x) & 63) != 0; x += 4)
+    _mm_stream_si128(reinterpret_cast<__m128i*>(out + x), _mm_loadu_si128(reinterpret_cast<const __m128i*>(b + x)));
+  for (; x + 16 <= n0; x += 16)
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(out + x), _mm512_loadu_si512(reinterpret_cast<const void*>(b + x)));
+  for (; x < n0; x += 4)
+    _mm_stream_si128(reinterpret_cast<__m128i*>(out + x), _mm_loadu_si128(reinterpret_cast<const __m128i*>(b + x)));
+}
+
 void fill_row_sse2(const int* L, const unsigned short* X, int n, int n0, int* b) {
   for (int k = 0; k < n; ++k) {
     const int a = std::min<int>(X[k], n0);
@@ -49,7 +61,9 @@ void run_decode_rows(const int* rows, const int* rlab, const unsigned short* rx,
     else
       fill_row_sse2(rlab + off, rx + off, n, n0, b);
     int32_t* out = dst + r * (long long)n0;
-    if (stream) {
+    if (stream && avx512) {
+      stream_row_avx512(out, b, n0);
+    } else if (stream) {
       for (int x = 0; x < n0; x += 4)
         _mm_stream_si128(reinterpret_cast<__m128i*>(out + x), _mm_load_si128(reinterpret_cast<const __m128i*>(b + x)));
     } else {

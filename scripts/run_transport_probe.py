@@ -23,7 +23,7 @@ sites = vx.SiteSet(vx.Kind.Voronoi, 3, pos, None, 0.0)
 out = torch.empty(n ** 3, dtype=torch.int32).pin_memory().numpy()
 hist = torch.zeros(ns, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
 settings = [dict(VX_D2H_RAW="1"), {}, dict(VX_D2H_THREADS="16"), dict(VX_D2H_THREADS="8"),
-            dict(VX_CHUNKS="8"), {}]
+            dict(VX_CHUNKS="8"), {}, {}]
 ref = None
 for st in settings:
     for k in ("VX_D2H_RAW", "VX_D2H_THREADS", "VX_CHUNKS"):
