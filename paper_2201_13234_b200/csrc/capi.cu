@@ -479,6 +479,7 @@ struct RunPlan {
   unsigned short* p_x = nullptr;
   unsigned long long* p_cnt = nullptr;  // mapped: written by launch_run_publish
   unsigned long long* d_pcnt = nullptr;  // its device address
+  int xbits = 0;  // > 0: packed runs, label << xbits | x (labelrun.cu)
   std::vector<RunChunk> chunks;
   std::vector<cudaEvent_t> enc, d2h;  // encoded (call stream), copied (copy stream)
   ~RunPlan() {
@@ -567,7 +568,7 @@ uint64_t run_drain(vx_context* ctx, RunPlan& rp, const int32_t* d_labels, int32_
       if (rtrace && t == 0) t_cp[c] = ms_now();
       const RunChunk& k = rp.chunks[c];
       run_decode_rows(reinterpret_cast<const int*>(rp.p_rows + k.r0), rp.p_lab + k.b0, rp.p_x + k.b0, k.rows * t / T, k.rows * (t + 1) / T, n0,
-                      out + k.r0 * n0, buf);
+                      rp.xbits, out + k.r0 * n0, buf);
       if (rtrace && t == 0) t_dec[c] = ms_now();
     }
   };
@@ -594,9 +595,10 @@ uint64_t run_drain(vx_context* ctx, RunPlan& rp, const int32_t* d_labels, int32_
                            ctx->copy_stream), "D2H label runs");
         ck(cudaMemcpyAsync(rp.p_lab + k.b0, rp.lab + k.b0, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->copy_stream),
            "D2H label runs");
-        ck(cudaMemcpyAsync(rp.p_x + k.b0, rp.x + k.b0, sizeof(unsigned short) * n, cudaMemcpyDeviceToHost,
-                           ctx->copy_stream), "D2H label runs");
-        bytes += sizeof(int2) * k.rows + 6 * n + 8;
+        if (rp.xbits == 0)
+          ck(cudaMemcpyAsync(rp.p_x + k.b0, rp.x + k.b0, sizeof(unsigned short) * n, cudaMemcpyDeviceToHost,
+                             ctx->copy_stream), "D2H label runs");
+        bytes += sizeof(int2) * k.rows + (rp.xbits ? 4 : 6) * n + 8;
       } else {  // short runs: the chunk's labels as they are
         m = 1;
         ck(cudaMemcpyAsync(out + k.r0 * n0, d_labels + k.r0 * n0, sizeof(int32_t) * k.rows * n0,
@@ -1129,7 +1131,14 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
       // the ball kernels put the last axis in gridDim.z (<= 65535 of 4..64
       // planes each): longer slabs are labelled in several launches
       cz = std::min<int64_t>(cz, kMaxZPlanes);
-      if (rle) run_plan_init(ctx, rp, nvs, g.n[0], (int)((nz + cz - 1) / cz));
+      if (rle) {
+        run_plan_init(ctx, rp, nvs, g.n[0], (int)((nz + cz - 1) / cz));
+        // label and first x in one word when every label (an original site
+        // index) fits beside the x bits
+        int xb = 1;
+        while ((1ll << xb) < g.n[0]) ++xb;
+        if ((long long)P->n_sites <= (1ll << (32 - xb)) && std::getenv("VX_RUN_UNPACKED") == nullptr) rp.xbits = xb;
+      }
       if ((pipelined || rle) && !ctx->copy_stream) {
         ck(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
         for (auto& e : ctx->chunk_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -1152,7 +1161,7 @@ int run(vx_context* ctx_in, const vx_problem* P, const vx_options* O_in, int32_t
           const RunChunk k{(c0 - zb) * plane / g.n[0], (c1 - c0) * plane / g.n[0], (c0 - zb) * plane / 4,
                            (c1 - c0) * plane / 4};
           launches += launch_run_encode(lb, k.rows, (int)g.n[0], rp.rows + k.r0, rp.lab + k.b0, rp.x + k.b0, k.cap,
-                                        rp.cnt + ci, st);
+                                        rp.cnt + ci, rp.xbits, st);
           launches += launch_run_publish(rp.cnt + ci, rp.d_pcnt + ci, st);
           ck(cudaEventRecord(rp.enc[ci], st), "run event");
           rp.chunks.push_back(k);

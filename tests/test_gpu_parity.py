@@ -480,7 +480,7 @@ def test_chunked_host_copies_identical(kind):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["sparse", "dense", "mixed", "odd_rows", "jm_np"])
+@pytest.mark.parametrize("case", ["sparse", "dense", "mixed", "odd_rows", "jm_np", "long_rows"])
 def test_run_coded_transport_identical(case):
     """Synchronous 3-D host-buffer calls move the label image across PCIe as
     runs along x and expand them on host threads (labelrun.cu); chunks whose
@@ -491,10 +491,12 @@ def test_run_coded_transport_identical(case):
     import paper_2201_13234_b200 as vx
     from paper_2201_13234_b200 import _lib
 
-    rng = np.random.default_rng({"sparse": 1, "dense": 2, "mixed": 3, "odd_rows": 4, "jm_np": 5}[case])
+    rng = np.random.default_rng({"sparse": 1, "dense": 2, "mixed": 3, "odd_rows": 4, "jm_np": 5, "long_rows": 6}[case])
     kind, periodic = (1, False) if case == "jm_np" else (0, True)
-    counts = {"odd_rows": [101, 130, 320]}.get(case, [160, 96, 300])
-    L = np.array([1.0, 0.6, 1.9]) if case != "odd_rows" else np.array([1.0, 1.3, 3.1])
+    # long_rows: 16 x bits leave 16 label bits, 70,000 sites do not fit -> 6-byte runs
+    counts = {"odd_rows": [101, 130, 320], "long_rows": [65535, 8, 9]}.get(case, [160, 96, 300])
+    L = {"odd_rows": np.array([1.0, 1.3, 3.1]), "long_rows": np.array([8.0, 0.005, 0.0055])}.get(
+        case, np.array([1.0, 0.6, 1.9]))
     nv = int(np.prod(counts))
     if case == "dense":
         ns = nv // 3
@@ -505,14 +507,14 @@ def test_run_coded_transport_identical(case):
         pos = np.concatenate([a, b])
         ns = len(pos)
     else:
-        ns = 3000
+        ns = 70000 if case == "long_rows" else 3000
         pos = rng.uniform(0, 1, (ns, 3)) * L
     pos = np.ascontiguousarray(np.minimum(pos, np.nextafter(L, 0)))
     t = rng.uniform(0, 0.05, ns) if kind == 1 else None
     box = vx.Domain(list(L), vx.Boundary.Periodic if periodic else vx.Boundary.NonPeriodic)
     grid = vx.VoxelGrid(counts, box)
     sites = vx.SiteSet(vx.Kind(kind), 3, pos, t, 1.0 if kind else 0.0)
-    old = {k: os.environ.get(k) for k in ("VX_D2H_RAW", "VX_CHUNKS")}
+    old = {k: os.environ.get(k) for k in ("VX_D2H_RAW", "VX_CHUNKS", "VX_RUN_UNPACKED")}
     res = {}
     try:
         os.environ["VX_D2H_RAW"] = "1"
@@ -526,6 +528,10 @@ def test_run_coded_transport_identical(case):
             res["pinned" + ch] = out.copy()
             res["pageable" + ch] = vx.tessellate_fast(sites, grid, distances=False).labels.labels.copy()
             run_bytes = int(_lib.lib().vx_last_d2h_bytes())
+        # the 6-byte runs (label, first x apart) that wide labels or long rows fall back to
+        os.environ["VX_RUN_UNPACKED"] = "1"
+        res["unpacked"] = vx.tessellate_fast(sites, grid, distances=False).labels.labels.copy()
+        unpacked_bytes = int(_lib.lib().vx_last_d2h_bytes())
     finally:
         for k, v in old.items():
             if v is None:
@@ -539,6 +545,10 @@ def test_run_coded_transport_identical(case):
         assert run_bytes >= 4 * nv  # every chunk raw
     else:
         assert run_bytes < 4 * nv * (0.8 if case == "mixed" else 0.5)
+        if case == "long_rows":
+            assert run_bytes == unpacked_bytes
+        else:
+            assert run_bytes < unpacked_bytes  # labels fit beside x: 4-byte runs
     # and the raw image itself against the device-pointer path
     from paper_2201_13234_b200.engine import Tessellator
 
