@@ -508,7 +508,8 @@ def run_ours(args):
                # of equal labels along x (expanded into `out` on host threads)
                "d2h_bytes_per_step": int(np.mean(d2h_bytes[1:])),
                "d2h_raw_bytes_per_step": int(4 * nvs + 8 * ns),
-               "ms_per_step": float(t_e2e.item()) * 1e3, "host_buffers": "pinned"}
+               "ms_per_step": float(t_e2e.item()) * 1e3, "host_buffers": "pinned",
+               "calls_ms": [round(1e3 * t, 2) for t in e2e_t[1:]]}
         if world == 1:
             fp = "%016x" % _lib.lib().vx_label_fingerprint(out.ctypes.data_as(_lib.C.c_void_p), out.size)
             out_h = out
