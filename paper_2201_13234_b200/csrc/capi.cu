@@ -550,6 +550,10 @@ uint64_t run_drain(vx_context* ctx, RunPlan& rp, const int32_t* d_labels, int32_
   std::condition_variable cv;
   int issued = 0;
   bool failed = false;
+  const long long kRowBlock = std::max<long long>(16, (1 << 18) / std::max(1, n0));  // ~1 MB of image
+  const bool run_static = std::getenv("VX_RUN_STATIC") != nullptr;  // A/B: the fixed row split
+  std::vector<std::atomic<long long>> next_row(nck);
+  for (auto& a : next_row) a.store(0, std::memory_order_relaxed);
   auto worker = [&](int t) {
     std::vector<int> buf;
     for (int c = 0; c < nck; ++c) {
@@ -567,8 +571,18 @@ uint64_t run_drain(vx_context* ctx, RunPlan& rp, const int32_t* d_labels, int32_
       }
       if (rtrace && t == 0) t_cp[c] = ms_now();
       const RunChunk& k = rp.chunks[c];
-      run_decode_rows(reinterpret_cast<const int*>(rp.p_rows + k.r0), rp.p_lab + k.b0, rp.p_x + k.b0, k.rows * t / T, k.rows * (t + 1) / T, n0,
-                      rp.xbits, out + k.r0 * n0, buf);
+      // blocks of rows claimed from the chunk's counter: no thread waits for a
+      // slower one, and the issuing thread joins once every chunk is issued
+      if (run_static) {
+        if (t < T)
+          run_decode_rows(reinterpret_cast<const int*>(rp.p_rows + k.r0), rp.p_lab + k.b0, rp.p_x + k.b0,
+                          k.rows * t / T, k.rows * (t + 1) / T, n0, rp.xbits, out + k.r0 * n0, buf);
+      } else for (;;) {
+        const long long r = next_row[c].fetch_add(kRowBlock, std::memory_order_relaxed);
+        if (r >= k.rows) break;
+        run_decode_rows(reinterpret_cast<const int*>(rp.p_rows + k.r0), rp.p_lab + k.b0, rp.p_x + k.b0, r,
+                        std::min<long long>(k.rows, r + kRowBlock), n0, rp.xbits, out + k.r0 * n0, buf);
+      }
       if (rtrace && t == 0) t_dec[c] = ms_now();
     }
   };
@@ -613,6 +627,7 @@ uint64_t run_drain(vx_context* ctx, RunPlan& rp, const int32_t* d_labels, int32_
       }
       cv.notify_all();
     }
+    worker(T);  // every chunk is issued: expand with the others
     for (auto& x : th) x.join();
     th.clear();
     bool bad = false;
