@@ -135,8 +135,10 @@ const char* vx_last_error(void);
 /* Bytes the calling thread's last vx_tessellate call moved device -> host
  * (host-buffer calls: label image, distances, histogram).  Synchronous 3-D
  * host-buffer calls without distances move the label image as runs of equal
- * labels along x (per x-row an 8-byte record, per run an int32 label and a
- * uint16 first x) and expand them into labels_out on host threads; chunks
+ * labels along x (per x-row an 8-byte record, per run one 32-bit word
+ * `label << xbits | first x` when the site indices fit beside the x bits,
+ * else an int32 label and a uint16 first x) and expand them into labels_out
+ * on host threads; chunks
  * whose runs average < 4 voxels are copied raw.  labels_out is identical
  * either way.  VX_D2H_RAW=1 forces the raw copy. */
 uint64_t vx_last_d2h_bytes(void);
